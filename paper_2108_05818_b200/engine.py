@@ -1,0 +1,460 @@
+"""The chunk-managed training step (iteration executor).
+
+Decision-identical restatement of `/root/reference/pkg/src/chunkstar/engine.py`:
+the 2E+1 moment grid, the rising edge (non-model footprint, gather, pin,
+fetch, ACCESS_FOR_COMPUTE, BWD grad staging), the during-event sample, the
+falling edge (FINISH_FWD / FINISH_BWD_GRAD_OVERWRITE + ``note_write``,
+unpin, DP release / reduce-scatter), the post-FWD reset and the
+per-position ADAM walk on the planned device (`engine.py:164-364`).
+
+Differences are structural, not behavioural:
+
+* the iteration is exposed as a *stepwise protocol* —
+  :meth:`Engine.begin_iteration`, :meth:`Engine.start_event`,
+  :meth:`Engine.finish_event`, :meth:`Engine.end_iteration` — so a real
+  model's module hooks can drive the very same decisions that
+  :meth:`Engine.run_iteration` drives from the timeline in
+  accounting-only mode;
+* an optional *executor* (see :class:`StepExecutor`; B200 implementation
+  in :mod:`.payload`) realises the physical work at the reference's
+  mutation points: parameter views before compute, the fused chunk Adam
+  (CUDA kernel ``cs_adam_chunks`` for GPU-placed positions, the host
+  kernel for CPU-placed ones) at the ADAM ``note_write``;
+* the reference's global location sweep over every chunk at every moment
+  (>90% of its run time) is replaced by a check over the chunks
+  that actually hold COMPUTE tensors, which is the same predicate.
+"""
+
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Sequence
+
+from .chunks import Chunk, ChunkKind, ChunkSet
+from .fsm import TensorState, Trigger
+from .memory import EvictionStrategy, MemoryManager, OOMError, TransferEvent
+from .model import (CPU, GPU, ModelSchema, OpKind, Phase, Timeline,
+                    activation_bytes_at)
+from .parallel import CollectiveEvent, DpRuntime
+from .profiler import MomentSample, PlacementPlan, WarmupStats
+
+EMBEDDING_LEDGER_ID = "embedding"
+
+
+class LocationConstraintError(AssertionError):
+    """A COMPUTE tensor's chunk was not resident on its compute device."""
+
+
+@dataclass
+class IterationReport:
+    iteration: int
+    warmup: bool
+    feasible: bool = True
+    failure_reason: Optional[str] = None
+    failure_moment: Optional[int] = None
+    samples: List[MomentSample] = field(default_factory=list)
+    transfers: List[TransferEvent] = field(default_factory=list)
+    collectives: List[CollectiveEvent] = field(default_factory=list)
+    cpu_to_gpu_bytes: int = 0
+    gpu_to_cpu_bytes: int = 0
+    intra_gpu_collective_bytes: int = 0
+    peak_gpu_bytes: int = 0
+    peak_cpu_bytes: int = 0
+
+    @property
+    def pcie_bytes(self) -> int:
+        return self.cpu_to_gpu_bytes + self.gpu_to_cpu_bytes
+
+    def validate_conservation(self) -> None:
+        moved = sum(t.bytes for t in self.transfers)
+        if moved != self.pcie_bytes:
+            raise AssertionError("transfer ledger does not balance: %d != %d"
+                                 % (self.pcie_bytes, moved))
+
+
+class StepExecutor:
+    """Physical side of the step (no-op base class = accounting only)."""
+
+    def on_compute_start(self, ev, chunks: Sequence[Chunk]) -> None:
+        pass
+
+    def on_compute_finish(self, ev, chunks: Sequence[Chunk]) -> None:
+        pass
+
+    def on_adam_begin(self, iteration: int) -> None:
+        pass
+
+    def init_optimizer_state(self, position: int, device: str) -> None:
+        pass
+
+    def adam_position(self, position: int, device: str) -> None:
+        pass
+
+    def retain_param_payload(self, chunk: Chunk, device: str) -> None:
+        pass
+
+    def on_adam_end(self) -> None:
+        pass
+
+
+@dataclass
+class _IterState:
+    report: IterationReport
+    stats: Optional[WarmupStats]
+    warmup: bool
+    plan_builder: Optional[Callable[[WarmupStats], PlacementPlan]]
+    local_positions: List[int]
+    transfers_before: int
+    c2g_before: int
+    g2c_before: int
+    coll_before: int
+    coll_bytes_before: int
+    next_event: int = 0
+    failed: bool = False
+
+
+class Engine:
+    """Runs iterations of one timeline against one chunk layout."""
+
+    def __init__(self, chunk_set: ChunkSet, timeline: Timeline,
+                 manager: MemoryManager, schema: Optional[ModelSchema] = None,
+                 dp: Optional[DpRuntime] = None,
+                 limit_fraction: float = 0.8,
+                 non_model_fn: Optional[Callable[[int], int]] = None,
+                 trace_fn: Optional[Callable[[dict], None]] = None,
+                 executor: Optional[StepExecutor] = None):
+        self.chunk_set = chunk_set
+        self.timeline = timeline
+        self.manager = manager
+        self.schema = schema
+        self.dp = dp
+        self.limit_fraction = limit_fraction
+        self.trace_fn = trace_fn
+        self.executor = executor
+        if non_model_fn is None:
+            if schema is not None:
+                ck = timeline.checkpointed
+                non_model_fn = lambda m: activation_bytes_at(schema, timeline, m, ck)
+            else:
+                non_model_fn = lambda m: 0
+        self.non_model_fn = non_model_fn
+        self.embedding_device = CPU
+        self.measured_strategy = manager.strategy
+        self.warmup_stats: Optional[WarmupStats] = None
+        self.plan: Optional[PlacementPlan] = None
+        self._computing: Dict[int, Chunk] = {}  # chunks holding COMPUTE tensors
+        self._it: Optional[_IterState] = None
+        self._check_single_gradient_write()
+
+    def _check_single_gradient_write(self) -> None:
+        """A tensor's grad overwrites its fp16 slot: ≤1 BWD event per tensor."""
+        writer: Dict[int, int] = {}
+        for ev in self.timeline.events:
+            if ev.phase is not Phase.BWD:
+                continue
+            for tid in ev.tensor_refs:
+                if tid in writer:
+                    raise ValueError("tensor %d written by backward events %d and %d"
+                                     % (tid, writer[tid], ev.index))
+                writer[tid] = ev.index
+
+    # -- checks and sampling ----------------------------------------------------
+
+    def _fp16_tensors(self, ev) -> List:
+        return [self.chunk_set.tensor(ChunkKind.PARAM_FP16, tid) for tid in ev.tensor_refs]
+
+    def _assert_location(self, chunks: Sequence[Chunk], device: str, moment: int) -> None:
+        for chunk in chunks:
+            computing = any(t.state is TensorState.COMPUTE for t in chunk.tensors)
+            if computing and not chunk.is_resident_on(device):
+                raise LocationConstraintError("chunk %d computes at moment %d but is not on %s"
+                                              % (chunk.chunk_id, moment, device))
+
+    def validate_locations(self, moment: int) -> None:
+        """Every chunk with a COMPUTE tensor has a resident copy."""
+        for chunk in self._computing.values():
+            if not chunk.copies and any(t.state is TensorState.COMPUTE
+                                        for t in chunk.tensors):
+                raise LocationConstraintError(
+                    "chunk %d has COMPUTE tensors but no residence at moment %d"
+                    % (chunk.chunk_id, moment))
+
+    def _sample(self, moment: int, label: str) -> None:
+        it = self._it
+        fresh = []
+        for pool in self.manager.pools.values():
+            model = pool.chunk_bytes + pool.extra_model_bytes
+            used = pool.used_bytes
+            fresh.append(MomentSample(moment=moment, device=pool.device, used_bytes=used,
+                                      chunk_bytes=model, non_model_bytes=used - model))
+        it.report.samples.extend(fresh)
+        if it.stats is not None:
+            it.stats.samples.extend(fresh)
+        self.validate_locations(moment)
+        if self.trace_fn is not None:
+            self.trace_fn({"moment": moment, "event": label,
+                           "device_usage": {p.device: p.used_bytes
+                                            for p in self.manager.pools.values()},
+                           "transfers": len(self.manager.transfers)})
+
+    def _edge(self, moment: int) -> None:
+        """Set the moment's non-model footprint; apply the warm-up soft limit."""
+        mgr = self.manager
+        mgr.set_non_model(GPU, self.non_model_fn(moment), moment)
+        if self._it.warmup:
+            cap = mgr.pools[GPU].capacity_bytes
+            mgr.enforce_soft_limit(GPU, int(self.limit_fraction * cap), moment)
+
+    def _soft_limit(self, moment: int) -> None:
+        if self._it.warmup:
+            cap = self.manager.pools[GPU].capacity_bytes
+            self.manager.enforce_soft_limit(GPU, int(self.limit_fraction * cap), moment)
+
+    # -- event bodies -------------------------------------------------------------
+
+    def _fire(self, tensors, trigger: Trigger) -> None:
+        for t in tensors:
+            t.fire(trigger)
+
+    def _compute_start(self, ev, moment: int, iteration: int) -> None:
+        tensors = self._fp16_tensors(ev)
+        chunks = self.chunk_set.param_chunks_for_tensors(ev.tensor_refs)
+        mgr = self.manager
+        if self.dp is not None:
+            self.dp.on_param_access(ev.phase, chunks, moment, iteration)
+        for chunk in chunks:
+            mgr.pin(chunk, GPU)
+            mgr.fetch_chunk(chunk, GPU, moment)
+            mgr.record_access(chunk, GPU, moment)
+        self._fire(tensors, Trigger.ACCESS_FOR_COMPUTE)
+        for chunk in chunks:
+            self._computing[chunk.chunk_id] = chunk
+        self._assert_location(chunks, GPU, moment)
+        if ev.phase is Phase.BWD and ev.param_bytes:
+            mgr.charge_temp(GPU, ev.param_bytes, moment)
+        stats = self._it.stats
+        if stats is not None:
+            stats.working_set_bytes = max(stats.working_set_bytes,
+                                          mgr.pinned_bytes(GPU))
+        if self.executor is not None:
+            self.executor.on_compute_start(ev, chunks)
+
+    def _compute_finish(self, ev, moment: int, iteration: int) -> None:
+        tensors = self._fp16_tensors(ev)
+        chunks = self.chunk_set.param_chunks_for_tensors(ev.tensor_refs)
+        mgr = self.manager
+        if self.executor is not None:
+            self.executor.on_compute_finish(ev, chunks)
+        if ev.phase is Phase.BWD:
+            self._fire(tensors, Trigger.FINISH_BWD_GRAD_OVERWRITE)
+            for chunk in chunks:
+                mgr.note_write(chunk, GPU)
+            if ev.param_bytes:
+                mgr.release_temp(GPU, ev.param_bytes)
+        else:
+            self._fire(tensors, Trigger.FINISH_FWD)
+        for chunk in chunks:
+            self._computing.pop(chunk.chunk_id, None)
+            mgr.unpin(chunk)
+        if self.dp is not None:
+            if ev.phase is Phase.FWD:
+                self.dp.after_fwd_event(chunks, moment)
+            elif ev.phase is Phase.BWD:
+                self.dp.after_bwd_event(chunks, moment, iteration)
+
+    def _embedding_start(self, ev, moment: int) -> None:
+        emb = self.chunk_set.embedding
+        if emb is None:
+            return
+        fwd = ev.phase is Phase.FWD
+        src, dst = (CPU, GPU) if fwd else (GPU, CPU)
+        if self.embedding_device == CPU:
+            nbytes = ev.activation_delta_bytes if fwd else -ev.activation_delta_bytes
+        else:
+            self.manager.charge_temp(GPU, emb.fp16_bytes, moment)
+            nbytes = emb.fp16_bytes
+        self.manager.record_extra_transfer(moment, EMBEDDING_LEDGER_ID, src, dst, nbytes)
+
+    def _embedding_finish(self, ev) -> None:
+        emb = self.chunk_set.embedding
+        if emb is not None and self.embedding_device == GPU:
+            self.manager.release_temp(GPU, emb.fp16_bytes)
+
+    def _adam(self, moment: int, plan: PlacementPlan, local_positions: Sequence[int],
+              iteration: int) -> None:
+        mgr, cs, ex = self.manager, self.chunk_set, self.executor
+        staging = ChunkKind.PARAM_FP32.elem_bytes * cs.capacity_elems
+        if ex is not None:
+            ex.on_adam_begin(iteration)
+        for pos in local_positions:
+            device = plan.device_of_position(pos)
+            triplet = cs.os_triplet(pos)
+            param = cs.param_chunk(pos)
+            born = False
+            for chunk in triplet:
+                mgr.pin(chunk, device)
+                if chunk.resident_device is None:
+                    # lazily initialised optimizer state is born on its
+                    # planned device: no wire traffic (engine.py:234-240)
+                    mgr.place_payload(chunk, device, moment)
+                    self._fire(chunk.tensors, Trigger.INIT)
+                    born = True
+                else:
+                    mgr.fetch_chunk(chunk, device, moment)
+                mgr.record_access(chunk, device, moment)
+            if born and ex is not None:
+                ex.init_optimizer_state(pos, device)
+            for chunk in triplet:
+                self._fire(chunk.tensors, Trigger.ADAM_ACCESS)
+                self._computing[chunk.chunk_id] = chunk
+            self._assert_location(triplet, device, moment)
+            mgr.pin(param, device)
+            if device not in param.copies:
+                mgr.fetch_chunk(param, device, moment, reason="adam_copy")
+            mgr.record_access(param, device, moment)
+            mgr.charge_temp(device, staging, moment)
+            if ex is not None:
+                ex.adam_position(pos, device)  # reads grads, writes p32/m/v/p16
+            for chunk in triplet:
+                mgr.note_write(chunk, device)
+            # grads consumed; the fp16 payload on `device` is reborn as the
+            # updated parameters (engine.py:256-263)
+            self._fire(param.tensors, Trigger.RELEASE)
+            if ex is not None:
+                ex.retain_param_payload(param, device)
+            mgr.release_chunk(param)
+            mgr.place_payload(param, device, moment)
+            self._fire(param.tensors, Trigger.ALLGATHER_ARRIVAL)
+            mgr.unpin(param)
+            if device != GPU:
+                mgr.fetch_chunk(param, GPU, moment, reason="adam_copy")
+            mgr.release_temp(device, staging)
+            for chunk in triplet:
+                self._fire(chunk.tensors, Trigger.ADAM_FINISH)
+                self._computing.pop(chunk.chunk_id, None)
+                mgr.unpin(chunk)
+        if ex is not None:
+            ex.on_adam_end()
+
+    def _post_fwd_reset(self) -> None:
+        for chunk in self.chunk_set.lists[ChunkKind.PARAM_FP16].chunks:
+            for t in chunk.tensors:
+                if t.lifecycle.state is TensorState.HOLD_AFTER_FWD:
+                    t.fire(Trigger.POST_FWD_RESET)
+
+    # -- stepwise protocol ------------------------------------------------------------
+
+    def begin_iteration(self, iteration: int, warmup: bool,
+                        plan_builder: Optional[Callable[[WarmupStats], PlacementPlan]] = None,
+                        local_positions: Optional[Sequence[int]] = None) -> IterationReport:
+        mgr = self.manager
+        report = IterationReport(iteration=iteration, warmup=warmup)
+        stats = None
+        if warmup:
+            mgr.strategy = EvictionStrategy.LIST_ORDER
+            mgr.recording = True
+            stats = WarmupStats()
+            stats.access_moments = mgr.access_moments
+            self.warmup_stats = stats
+        else:
+            mgr.strategy = self.measured_strategy
+            mgr.recording = False
+        if local_positions is None:
+            local_positions = (self.dp.partition.local_positions(self.dp.rank)
+                               if self.dp is not None
+                               else list(range(self.chunk_set.positions)))
+        dp = self.dp
+        self._it = _IterState(report=report, stats=stats, warmup=warmup,
+                              plan_builder=plan_builder,
+                              local_positions=list(local_positions),
+                              transfers_before=len(mgr.transfers),
+                              c2g_before=mgr.cpu_to_gpu_bytes,
+                              g2c_before=mgr.gpu_to_cpu_bytes,
+                              coll_before=len(dp.events) if dp else 0,
+                              coll_bytes_before=dp.collective_bytes if dp else 0)
+        for pool in mgr.pools.values():
+            pool.peak_bytes = pool.used_bytes
+        self._guarded(lambda: (self._edge(0), self._sample(0, "start")))
+        return report
+
+    def _guarded(self, fn) -> None:
+        it = self._it
+        if it.failed:
+            return
+        try:
+            fn()
+        except OOMError as oom:
+            it.failed = True
+            it.report.feasible = False
+            it.report.failure_reason = "GPU_OOM" if oom.device == GPU else "CPU_OOM"
+            it.report.failure_moment = oom.moment
+
+    def start_event(self, ev) -> None:
+        """Rising edge of event ``ev`` plus the during-event sample."""
+        it = self._it
+        if ev.index != it.next_event:
+            raise RuntimeError("event %s arrived out of timeline order (expected #%d)"
+                               % (ev.name, it.next_event))
+        self._guarded(lambda: self._start_body(ev))
+
+    def _start_body(self, ev) -> None:
+        it = self._it
+        m = 2 * ev.index + 1
+        self.manager.set_non_model(GPU, self.non_model_fn(m), m)
+        if ev.phase is Phase.ADAM:
+            if it.plan_builder is not None:
+                self.plan = it.plan_builder(it.stats)
+            if self.plan is None:
+                raise ValueError("optimizer event needs a placement plan")
+            self._adam(m, self.plan, it.local_positions, it.report.iteration)
+        elif ev.kind is OpKind.EMBEDDING:
+            self._embedding_start(ev, m)
+        else:
+            self._compute_start(ev, m, it.report.iteration)
+        self._soft_limit(m)
+        self._sample(m, ev.name)
+
+    def finish_event(self, ev) -> None:
+        """Falling edge of ``ev`` plus the boundary sample after it."""
+        self._guarded(lambda: self._finish_body(ev))
+        self._it.next_event = ev.index + 1
+
+    def _finish_body(self, ev) -> None:
+        m = 2 * ev.index + 1
+        if ev.kind is OpKind.EMBEDDING:
+            self._embedding_finish(ev)
+        elif ev.phase is not Phase.ADAM:
+            self._compute_finish(ev, m, self._it.report.iteration)
+        if ev.index == self.timeline.last_fwd_index:
+            self._post_fwd_reset()
+        self._edge(m + 1)
+        self._sample(m + 1, ev.name + ".end")
+
+    def end_iteration(self) -> IterationReport:
+        it, mgr, dp = self._it, self.manager, self.dp
+        report = it.report
+        report.transfers = mgr.transfers[it.transfers_before:]
+        report.cpu_to_gpu_bytes = mgr.cpu_to_gpu_bytes - it.c2g_before
+        report.gpu_to_cpu_bytes = mgr.gpu_to_cpu_bytes - it.g2c_before
+        if dp is not None:
+            report.collectives = dp.events[it.coll_before:]
+            report.intra_gpu_collective_bytes = dp.collective_bytes - it.coll_bytes_before
+        report.peak_gpu_bytes = mgr.pools[GPU].peak_bytes
+        report.peak_cpu_bytes = mgr.pools[CPU].peak_bytes
+        report.validate_conservation()
+        self._it = None
+        return report
+
+    @property
+    def iteration_failed(self) -> bool:
+        return self._it is not None and self._it.failed
+
+    def run_iteration(self, iteration: int, warmup: bool,
+                      plan_builder: Optional[Callable[[WarmupStats], PlacementPlan]] = None,
+                      local_positions: Optional[Sequence[int]] = None) -> IterationReport:
+        """Accounting-only iteration driven straight from the timeline."""
+        self.begin_iteration(iteration, warmup, plan_builder, local_positions)
+        for ev in self.timeline.events:
+            if self._it.failed:
+                break
+            self.start_event(ev)
+            self.finish_event(ev)
+        return self.end_iteration()
