@@ -1,0 +1,176 @@
+/*
+ * chunkstar_b200.h — C ABI of libchunkstar_b200.so, the B200 (sm_100a)
+ * kernels behind the chunk-managed training step.
+ *
+ * The reference (`/root/reference/pkg/src/chunkstar`) has no FFI: its hot
+ * path is a Python object API whose "kernels" are byte-accounting calls.
+ * Each entry point below realises one of those accounting sites; the
+ * Python engine (paper_2108_05818_b200.engine / .payload) calls them at
+ * exactly the point the reference charges the bytes.
+ *
+ * Conventions
+ *  - plain C types only; device pointers are void* / float*, sizes int64_t;
+ *  - every GPU entry point takes a cudaStream_t (passed as void*) and is
+ *    asynchronous; the library never allocates, frees or synchronises
+ *    device memory (the caller owns all buffers);
+ *  - return 0 on success, a cudaError_t (>0) from the launch, or a
+ *    negative CS_E* argument error; cs_last_error() describes the last
+ *    failure on the calling thread;
+ *  - dtype codes: CS_FP16 = 0, CS_BF16 = 1, CS_FP32 = 2 (sources only).
+ *
+ * Numerics (bit-identical in the CUDA kernels, the host kernel and the C
+ * oracle; the association is torch.optim.Adam's CPU single-tensor path —
+ * lerp/addcmul/addcdiv — with IEEE sqrt and division).  Scalars are formed
+ * in double and rounded once: b2 = f(beta2), c1 = f(1-beta1),
+ * c2 = f(1-beta2), decay = f(1 - lr*wd), wd, eps.  Per element, with
+ * s = step scalars (CsStepState) and fma = fused multiply-add:
+ *     g  = float(g16) * s.grad_scale
+ *     if wd != 0:  adamw ? p = p * decay  :  g = fma(wd, p, g)
+ *     m  = fma(c1, g - m, m)                      (lerp)
+ *     v  = fma(c2 * g, g, v * b2)                 (mul_ + addcmul_)
+ *     p  = p + ((-s.step_size) * m) / (sqrt(v) / s.sqrt_bc2 + eps)
+ *     p16 = round_to_nearest_even(p)
+ * When s.skip != 0 (non-finite gradients) nothing is written.
+ */
+#ifndef CHUNKSTAR_B200_H
+#define CHUNKSTAR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { CS_FP16 = 0, CS_BF16 = 1, CS_FP32 = 2 };
+
+enum {
+  CS_OK = 0,
+  CS_EINVAL = -1,      /* bad argument (null pointer, negative count, dtype) */
+  CS_EALIGN = -2,      /* a vectorised buffer is not 16-byte aligned */
+  CS_ETOOMANY = -3     /* work list longer than CS_MAX_ITEMS */
+};
+
+#define CS_MAX_ITEMS 4096
+
+/* Adam hyper-parameters (host struct, passed by pointer, copied at launch). */
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay;
+  int32_t adamw;           /* 1: decoupled weight decay (AdamW) */
+} CsAdamHyper;
+
+/* Per-step optimizer scalars; lives in DEVICE memory (64 bytes) and is
+ * advanced on the device by cs_adam_prepare, so a step needs no host sync.
+ * Initialise with cs_step_state_init. */
+typedef struct {
+  double  beta1_pow;       /* beta1^t after the last applied step */
+  double  beta2_pow;
+  int64_t step;            /* applied (non-skipped) steps */
+  float   loss_scale;      /* dynamic loss scale used for THIS step's grads */
+  int32_t good_steps;      /* consecutive finite steps since last growth */
+  float   grad_scale;      /* out: (1/loss_scale) * clip_coef */
+  float   step_size;       /* out: lr / (1 - beta1^t) */
+  float   sqrt_bc2;        /* out: sqrt(1 - beta2^t) */
+  int32_t skip;            /* out: 1 if the step is skipped (inf/nan) */
+  float   grad_norm;       /* out: unscaled global L2 norm */
+  float   sumsq;           /* in: global sum of squares of the scaled grads */
+} CsStepState;
+
+/* One fused-Adam work item: the used prefix [0, n) of one chunk position
+ * (or of a non-chunked buffer such as the embedding).
+ * p16: the fp16/bf16 chunk payload — holds the gradients on entry and the
+ *      updated parameters on exit (grads reuse the param chunk, PAPER §4).
+ * p32, m, v: the fp32 optimizer-state triplet of the same position. */
+typedef struct {
+  void*   p16;
+  float*  p32;
+  float*  m;
+  float*  v;
+  int64_t n;
+} CsAdamItem;
+
+/* One grad-reduction item: n elements of fp16/bf16 gradients. */
+typedef struct {
+  const void* g16;
+  int64_t n;
+} CsGradItem;
+
+/* One pack / cast item: dst = chunk + offset (elements of dst dtype). */
+typedef struct {
+  void*       chunk;
+  int64_t     offset;
+  const void* src;
+  int64_t     n;
+} CsPackItem;
+
+/* ---- library ------------------------------------------------------------ */
+const char* cs_version(void);
+const char* cs_last_error(void);
+/* number of kernels this library has launched (process lifetime) */
+int64_t     cs_launch_count(void);
+/* number of SMs of the current device (grid sizing), or <0 on error */
+int         cs_num_sms(void);
+
+/* ---- K1: fused chunk Adam -------------------------------------------------
+ * Replaces the accounting of Engine._adam_event for a GPU-placed position
+ * (`/root/reference/pkg/src/chunkstar/engine.py:225-272`: charge_temp of one
+ * fp32 staging chunk :227/:253, note_write of the triplet :254-255, param
+ * release + place_payload :257-263).  One launch covers any number of
+ * positions (grid-stride over all items, 128-bit loads/stores). */
+int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
+                   const CsAdamHyper* hyper, const CsStepState* d_state,
+                   void* stream);
+
+/* ---- K2: gradient sum of squares -------------------------------------------
+ * Global grad-norm / found-inf for clipping and dynamic loss scaling (no
+ * reference counterpart: the simulator has no numerics).  Writes one fp32
+ * partial per block into d_partials[0..n_partials) (n_partials must equal
+ * cs_sumsq_partials()); cs_sumsq_finalize reduces them in a fixed order
+ * (deterministic) into d_state->sumsq (accumulate=1 adds to it). */
+int cs_sumsq_partials(void);
+int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
+                  float* d_partials, void* stream);
+int cs_sumsq_finalize(const float* d_partials, int n_partials,
+                      CsStepState* d_state, int accumulate, void* stream);
+
+/* ---- step scalars -------------------------------------------------------------
+ * Device-side: consume d_state->sumsq, decide skip, clip coefficient,
+ * bias corrections and the dynamic loss-scale update (growth/backoff). */
+int cs_step_state_init(CsStepState* d_state, float init_loss_scale, void* stream);
+int cs_adam_prepare(CsStepState* d_state, const CsAdamHyper* hyper,
+                    float max_grad_norm, float growth_factor, float backoff_factor,
+                    int32_t growth_interval, int32_t dynamic_scale, void* stream);
+
+/* ---- K3 / K4: tensor -> chunk slot pack (grad overwrite / accumulate) -----
+ * Realises the BWD grad overwrite of Engine._finish_compute_event
+ * (`engine.py:177-190`: charge_temp(param_bytes), FINISH_BWD_GRAD_OVERWRITE,
+ * note_write).  accumulate=0: slot = src (K3); 1: slot += src (K4).
+ * Offsets need not be aligned (gap-free packing, `chunks.py:186-200`). */
+int cs_pack(const CsPackItem* items, int n_items, int dtype, int accumulate,
+            void* stream);
+
+/* ---- K5: fp32 -> fp16/bf16 cast + pack -----------------------------------------
+ * Materialises fp16 param chunks from fp32 init weights
+ * (`chunks.py:297-314` init_on_cpu, `scenario.py:126`). src is fp32. */
+int cs_cast_pack(const CsPackItem* items, int n_items, int dtype, void* stream);
+
+/* ---- K6: optimizer-state birth ---------------------------------------------------
+ * Lazy OS materialisation at the first ADAM on the planned device
+ * (`engine.py:234-240`): p32 = float(src), m = v = 0.  src_dtype is
+ * CS_FP16/CS_BF16 (widen the fp16 params) or CS_FP32 (copy master init). */
+int cs_master_init(float* p32, float* m, float* v, const void* src, int src_dtype,
+                   int64_t n, void* stream);
+
+/* ---- host Adam for CPU-placed positions (PAPER §5 device-aware placement) ----
+ * The placement plan may keep an optimizer triplet on the CPU
+ * (`profiler.py:93-130`); the reference then moves grads D2H and new params
+ * H2D as `adam_copy` (`engine.py:249-251, 265-267`).  This is the host
+ * kernel that runs there (AVX2/F16C + OpenMP, same rounding as K1).
+ * `state` is a HOST copy of the step scalars. Synchronous. */
+int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
+                        const CsAdamHyper* hyper, const CsStepState* state,
+                        int n_threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHUNKSTAR_B200_H */

@@ -1,0 +1,486 @@
+// K1 fused chunk Adam, K2 gradient sum-of-squares and the device-side step
+// scalars for the chunk-managed training step on B200 (sm_100a).
+//
+// K1 realises Engine._adam_event's per-position update
+// (/root/reference/pkg/src/chunkstar/engine.py:225-272): it reads the fp16
+// grad chunk and the fp32 master/momentum/variance chunks of a position and
+// writes fp32 state plus the new fp16 params back into the same fp16 chunk,
+// in one pass — 28 B/element of HBM traffic, the algorithmic minimum.
+//
+// Layout/access: every item is the used prefix [0, n) of one chunk payload
+// (chunk bases are allocation-aligned, tensors are packed gap-free, so the
+// prefix is one contiguous run).  A block tile is 256 threads x 4 groups x 4
+// elements = 4096 elements; in each group a warp touches 32 consecutive
+// 4-element groups, so every load/store instruction is a fully coalesced
+// 256 B (fp16, 64-bit/lane) or 512 B (fp32, 128-bit/lane) transaction.  All
+// 16 groups' loads of a thread are issued before any math (memory-level
+// parallelism ~ 14 x 16 B in flight per thread).  Data is touched exactly
+// once, so loads/stores carry the streaming (evict-first) policy.  The grid
+// is persistent: #SMs x resident blocks, striding over the block tiles of all
+// items of the launch (one launch updates every GPU-placed position).
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <math.h>
+
+#include "cs_internal.h"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kGroups = 4;   // 4-element groups per thread per block tile
+constexpr int kBlockTile = kThreads * kGroups * 4;
+
+struct AdamBatch {
+  CsAdamItem item[cs::kMaxBatch];
+  int64_t tile_start[cs::kMaxBatch + 1];  // exclusive prefix of block tiles
+  int n;
+  float b2, c1, c2, eps, wd, decay;  // scalars formed in double, rounded once
+  int adamw;
+};
+
+struct GradBatch {
+  CsGradItem item[cs::kMaxBatch];
+  int64_t tile_start[cs::kMaxBatch + 1];
+  int n;
+  int accumulate;  // 0: first batch of a call overwrites the partials
+};
+
+// ---- 16-bit storage helpers (4 elements = 64 bits) -------------------------
+
+template <int DT>
+__device__ __forceinline__ float4 widen4(uint2 w);
+template <>
+__device__ __forceinline__ float4 widen4<CS_FP16>(uint2 w) {
+  float2 a = __half22float2(*reinterpret_cast<__half2*>(&w.x));
+  float2 b = __half22float2(*reinterpret_cast<__half2*>(&w.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+template <>
+__device__ __forceinline__ float4 widen4<CS_BF16>(uint2 w) {
+  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w.x));
+  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <int DT>
+__device__ __forceinline__ uint2 narrow4(float4 f);
+template <>
+__device__ __forceinline__ uint2 narrow4<CS_FP16>(float4 f) {
+  __half2 a = __floats2half2_rn(f.x, f.y), b = __floats2half2_rn(f.z, f.w);
+  return make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+}
+template <>
+__device__ __forceinline__ uint2 narrow4<CS_BF16>(float4 f) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(f.x, f.y), b = __floats2bfloat162_rn(f.z, f.w);
+  return make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+}
+
+template <int DT>
+__device__ __forceinline__ float widen1(uint16_t h) {
+  if (DT == CS_FP16) return __half2float(__ushort_as_half(h));
+  return __bfloat162float(__ushort_as_bfloat16(h));
+}
+template <int DT>
+__device__ __forceinline__ uint16_t narrow1(float f) {
+  if (DT == CS_FP16) return __half_as_ushort(__float2half_rn(f));
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+// ---- the Adam element update (every op individually rounded) --------------
+
+struct AdamConsts {
+  float grad_scale, neg_step_size, sqrt_bc2;
+  float b2, c1, c2, eps, wd, decay;
+  bool adamw;
+};
+
+// Association of torch.optim.Adam's CPU single-tensor path (lerp_, mul_ +
+// addcmul_, addcdiv_), IEEE sqrt/div; see include/chunkstar_b200.h.
+__device__ __forceinline__ void adam1(float g16, float& p, float& m, float& v,
+                                      const AdamConsts& c) {
+  float g = __fmul_rn(g16, c.grad_scale);
+  if (c.wd != 0.0f) {
+    if (c.adamw) p = __fmul_rn(p, c.decay);
+    else g = __fmaf_rn(c.wd, p, g);
+  }
+  m = __fmaf_rn(c.c1, __fsub_rn(g, m), m);
+  v = __fmaf_rn(__fmul_rn(c.c2, g), g, __fmul_rn(v, c.b2));
+  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.sqrt_bc2), c.eps);
+  p = __fadd_rn(p, __fdiv_rn(__fmul_rn(c.neg_step_size, m), denom));
+}
+
+__device__ __forceinline__ int find_item(const int64_t* start, int n, int64_t tile) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+adam_chunks_kernel(const __grid_constant__ AdamBatch b, const CsStepState* __restrict__ st) {
+  if (st->skip) return;  // non-finite gradients: the whole step is skipped
+  AdamConsts c;
+  c.grad_scale = st->grad_scale;
+  c.neg_step_size = -st->step_size;
+  c.sqrt_bc2 = st->sqrt_bc2;
+  c.b2 = b.b2;
+  c.c1 = b.c1;
+  c.c2 = b.c2;
+  c.eps = b.eps;
+  c.wd = b.wd;
+  c.decay = b.decay;
+  c.adamw = b.adamw != 0;
+
+  const int64_t total = b.tile_start[b.n];
+  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int k = find_item(b.tile_start, b.n, tile);
+    const CsAdamItem it = b.item[k];
+    const int64_t base = (tile - b.tile_start[k]) * kBlockTile;
+    uint16_t* __restrict__ p16 = static_cast<uint16_t*>(it.p16);
+
+    if (base + kBlockTile <= it.n) {  // full tile: vector path
+      uint2 g[kGroups];
+      float4 p[kGroups], m[kGroups], v[kGroups];
+#pragma unroll
+      for (int u = 0; u < kGroups; ++u) {
+        const int64_t e = base + (int64_t)(u * kThreads + threadIdx.x) * 4;
+        g[u] = __ldcs(reinterpret_cast<const uint2*>(p16 + e));
+        p[u] = __ldcs(reinterpret_cast<const float4*>(it.p32 + e));
+        m[u] = __ldcs(reinterpret_cast<const float4*>(it.m + e));
+        v[u] = __ldcs(reinterpret_cast<const float4*>(it.v + e));
+      }
+#pragma unroll
+      for (int u = 0; u < kGroups; ++u) {
+        const float4 gf = widen4<DT>(g[u]);
+        adam1(gf.x, p[u].x, m[u].x, v[u].x, c);
+        adam1(gf.y, p[u].y, m[u].y, v[u].y, c);
+        adam1(gf.z, p[u].z, m[u].z, v[u].z, c);
+        adam1(gf.w, p[u].w, m[u].w, v[u].w, c);
+        const int64_t e = base + (int64_t)(u * kThreads + threadIdx.x) * 4;
+        __stcs(reinterpret_cast<float4*>(it.p32 + e), p[u]);
+        __stcs(reinterpret_cast<float4*>(it.m + e), m[u]);
+        __stcs(reinterpret_cast<float4*>(it.v + e), v[u]);
+        __stcs(reinterpret_cast<uint2*>(p16 + e), narrow4<DT>(p[u]));
+      }
+    } else {  // the last, partial tile of an item
+      for (int u = 0; u < kGroups; ++u) {
+        const int64_t e0 = base + (int64_t)(u * kThreads + threadIdx.x) * 4;
+        for (int64_t e = e0; e < e0 + 4 && e < it.n; ++e) {
+          float pp = it.p32[e], mm = it.m[e], vv = it.v[e];
+          adam1(widen1<DT>(p16[e]), pp, mm, vv, c);
+          it.p32[e] = pp;
+          it.m[e] = mm;
+          it.v[e] = vv;
+          p16[e] = narrow1<DT>(pp);
+        }
+      }
+    }
+  }
+}
+
+// ---- K2: sum of squares of fp16/bf16 gradients -----------------------------
+
+__device__ __forceinline__ float block_sum(float x) {
+  __shared__ float warp_sums[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) warp_sums[warp] = x;
+  __syncthreads();
+  float s = 0.0f;
+  if (warp == 0) {
+    s = lane < kThreads / 32 ? warp_sums[lane] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return s;  // valid in thread 0
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+grad_sumsq_kernel(const __grid_constant__ GradBatch b, float* __restrict__ partials) {
+  float acc = 0.0f;
+  const int64_t total = b.tile_start[b.n];
+  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int k = find_item(b.tile_start, b.n, tile);
+    const CsGradItem it = b.item[k];
+    const int64_t base = (tile - b.tile_start[k]) * kBlockTile;
+    const uint16_t* __restrict__ g16 = static_cast<const uint16_t*>(it.g16);
+    if (base + kBlockTile <= it.n) {
+      uint2 g[kGroups];
+#pragma unroll
+      for (int u = 0; u < kGroups; ++u)
+        g[u] = __ldcs(reinterpret_cast<const uint2*>(
+            g16 + base + (int64_t)(u * kThreads + threadIdx.x) * 4));
+#pragma unroll
+      for (int u = 0; u < kGroups; ++u) {
+        const float4 f = widen4<DT>(g[u]);
+        acc += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+      }
+    } else {
+      for (int u = 0; u < kGroups; ++u) {
+        const int64_t e0 = base + (int64_t)(u * kThreads + threadIdx.x) * 4;
+        for (int64_t e = e0; e < e0 + 4 && e < it.n; ++e) {
+          const float f = widen1<DT>(g16[e]);
+          acc += f * f;
+        }
+      }
+    }
+  }
+  const float s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = b.accumulate ? partials[blockIdx.x] + s : s;
+}
+
+__global__ void __launch_bounds__(kThreads)
+sumsq_finalize_kernel(const float* __restrict__ partials, int n, CsStepState* st,
+                      int accumulate) {
+  __shared__ double red[kThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += kThreads) acc += (double)partials[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {  // fixed-order tree: deterministic
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const float total = (float)red[0];
+    st->sumsq = accumulate ? st->sumsq + total : total;
+  }
+}
+
+__global__ void step_state_init_kernel(CsStepState* st, float loss_scale) {
+  st->beta1_pow = 1.0;
+  st->beta2_pow = 1.0;
+  st->step = 0;
+  st->loss_scale = loss_scale;
+  st->good_steps = 0;
+  st->grad_scale = __fdiv_rn(1.0f, loss_scale);
+  st->step_size = 0.0f;
+  st->sqrt_bc2 = 1.0f;
+  st->skip = 0;
+  st->grad_norm = 0.0f;
+  st->sumsq = 0.0f;
+}
+
+// One thread: skip decision, clip coefficient, bias corrections and the
+// dynamic loss-scale update, all from the device-resident sumsq.
+__global__ void adam_prepare_kernel(CsStepState* st, CsAdamHyper h, float max_norm,
+                                    float growth, float backoff, int32_t interval,
+                                    int32_t dynamic_scale) {
+  const float sumsq = st->sumsq;
+  const float ls = st->loss_scale;
+  if (!isfinite(sumsq)) {
+    st->skip = 1;
+    st->grad_norm = sumsq;
+    if (dynamic_scale) {
+      st->loss_scale = __fmul_rn(ls, backoff);
+      st->good_steps = 0;
+    }
+    return;
+  }
+  const float norm = __fdiv_rn(__fsqrt_rn(sumsq), ls);
+  float clip = 1.0f;
+  if (max_norm > 0.0f) clip = fminf(__fdiv_rn(max_norm, __fadd_rn(norm, 1e-6f)), 1.0f);
+  st->grad_scale = __fmul_rn(__fdiv_rn(1.0f, ls), clip);
+  st->grad_norm = norm;
+  st->skip = 0;
+  st->step += 1;
+  st->beta1_pow = __dmul_rn(st->beta1_pow, h.beta1);
+  st->beta2_pow = __dmul_rn(st->beta2_pow, h.beta2);
+  st->step_size = (float)__ddiv_rn(h.lr, __dsub_rn(1.0, st->beta1_pow));
+  st->sqrt_bc2 = (float)__dsqrt_rn(__dsub_rn(1.0, st->beta2_pow));
+  if (dynamic_scale && ++st->good_steps >= interval) {
+    st->loss_scale = __fmul_rn(ls, growth);
+    st->good_steps = 0;
+  }
+}
+
+// ---- host side ---------------------------------------------------------------
+
+int g_num_sms = 0;
+int g_adam_blocks_per_sm = 0;
+
+int num_sms() {
+  if (g_num_sms > 0) return g_num_sms;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return -1;
+  return g_num_sms;
+}
+
+bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+int launch_error(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cs::set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return (int)e;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" int cs_num_sms(void) { return num_sms(); }
+
+extern "C" int cs_sumsq_partials(void) {
+  const int sms = num_sms();
+  return sms > 0 ? sms * 4 : -1;
+}
+
+extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
+                              const CsAdamHyper* hyper, const CsStepState* d_state,
+                              void* stream) {
+  if (n_items < 0 || (n_items > 0 && !items) || !hyper || !d_state ||
+      (dtype != CS_FP16 && dtype != CS_BF16)) {
+    cs::set_error("cs_adam_chunks: invalid argument");
+    return CS_EINVAL;
+  }
+  const int sms = num_sms();
+  if (sms <= 0) {
+    cs::set_error("cs_adam_chunks: no CUDA device");
+    return CS_EINVAL;
+  }
+  if (g_adam_blocks_per_sm == 0) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, adam_chunks_kernel<CS_FP16>, kThreads, 0);
+    g_adam_blocks_per_sm = nb > 0 ? nb : 1;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int first = 0; first < n_items; first += cs::kMaxBatch) {
+    AdamBatch b;
+    b.n = 0;
+    int64_t tiles = 0;
+    for (int i = first; i < n_items && b.n < cs::kMaxBatch; ++i) {
+      const CsAdamItem& it = items[i];
+      if (it.n < 0 || (it.n > 0 && (!it.p16 || !it.p32 || !it.m || !it.v))) {
+        cs::set_error("cs_adam_chunks: item %d invalid", i);
+        return CS_EINVAL;
+      }
+      if (!aligned(it.p16, 8) || !aligned(it.p32, 16) || !aligned(it.m, 16) ||
+          !aligned(it.v, 16)) {
+        cs::set_error("cs_adam_chunks: item %d misaligned (p16 needs 8 B, fp32 16 B)", i);
+        return CS_EALIGN;
+      }
+      if (it.n == 0) continue;
+      b.item[b.n] = it;
+      b.tile_start[b.n] = tiles;
+      tiles += (it.n + kBlockTile - 1) / kBlockTile;
+      ++b.n;
+    }
+    b.tile_start[b.n] = tiles;
+    if (b.n == 0) continue;
+    b.b2 = (float)hyper->beta2;
+    b.c1 = (float)(1.0 - hyper->beta1);
+    b.c2 = (float)(1.0 - hyper->beta2);
+    b.eps = (float)hyper->eps;
+    b.wd = (float)hyper->weight_decay;
+    b.decay = (float)(1.0 - hyper->lr * hyper->weight_decay);
+    b.adamw = hyper->adamw;
+    const int64_t grid64 = (int64_t)sms * g_adam_blocks_per_sm;
+    const int grid = (int)(tiles < grid64 ? tiles : grid64);
+    if (dtype == CS_FP16)
+      adam_chunks_kernel<CS_FP16><<<grid, kThreads, 0, s>>>(b, d_state);
+    else
+      adam_chunks_kernel<CS_BF16><<<grid, kThreads, 0, s>>>(b, d_state);
+    cs::note_launches(1);
+    if (int e = launch_error("cs_adam_chunks")) return e;
+  }
+  return 0;
+}
+
+extern "C" int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
+                             float* d_partials, void* stream) {
+  if (n_items < 0 || (n_items > 0 && !items) || !d_partials ||
+      (dtype != CS_FP16 && dtype != CS_BF16)) {
+    cs::set_error("cs_grad_sumsq: invalid argument");
+    return CS_EINVAL;
+  }
+  const int grid = cs_sumsq_partials();
+  if (grid <= 0) {
+    cs::set_error("cs_grad_sumsq: no CUDA device");
+    return CS_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int first = 0;
+  bool wrote = false;
+  do {
+    GradBatch b;
+    b.n = 0;
+    b.accumulate = wrote ? 1 : 0;
+    int64_t tiles = 0;
+    for (int i = first; i < n_items && b.n < cs::kMaxBatch; ++i) {
+      const CsGradItem& it = items[i];
+      if (it.n < 0 || (it.n > 0 && !it.g16)) {
+        cs::set_error("cs_grad_sumsq: item %d invalid", i);
+        return CS_EINVAL;
+      }
+      if (!aligned(it.g16, 8)) {
+        cs::set_error("cs_grad_sumsq: item %d misaligned", i);
+        return CS_EALIGN;
+      }
+      if (it.n == 0) continue;
+      b.item[b.n] = it;
+      b.tile_start[b.n] = tiles;
+      tiles += (it.n + kBlockTile - 1) / kBlockTile;
+      ++b.n;
+    }
+    b.tile_start[b.n] = tiles;
+    // launched even when empty so the partials are (re)initialised
+    if (dtype == CS_FP16)
+      grad_sumsq_kernel<CS_FP16><<<grid, kThreads, 0, s>>>(b, d_partials);
+    else
+      grad_sumsq_kernel<CS_BF16><<<grid, kThreads, 0, s>>>(b, d_partials);
+    cs::note_launches(1);
+    if (int e = launch_error("cs_grad_sumsq")) return e;
+    wrote = true;
+    first += cs::kMaxBatch;
+  } while (first < n_items);
+  return 0;
+}
+
+extern "C" int cs_sumsq_finalize(const float* d_partials, int n_partials,
+                                 CsStepState* d_state, int accumulate, void* stream) {
+  if (!d_partials || n_partials <= 0 || !d_state) {
+    cs::set_error("cs_sumsq_finalize: invalid argument");
+    return CS_EINVAL;
+  }
+  sumsq_finalize_kernel<<<1, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_partials, n_partials, d_state, accumulate);
+  cs::note_launches(1);
+  return launch_error("cs_sumsq_finalize");
+}
+
+extern "C" int cs_step_state_init(CsStepState* d_state, float init_loss_scale, void* stream) {
+  if (!d_state || !(init_loss_scale > 0.0f)) {
+    cs::set_error("cs_step_state_init: invalid argument");
+    return CS_EINVAL;
+  }
+  step_state_init_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_state,
+                                                                        init_loss_scale);
+  cs::note_launches(1);
+  return launch_error("cs_step_state_init");
+}
+
+extern "C" int cs_adam_prepare(CsStepState* d_state, const CsAdamHyper* hyper,
+                               float max_grad_norm, float growth_factor,
+                               float backoff_factor, int32_t growth_interval,
+                               int32_t dynamic_scale, void* stream) {
+  if (!d_state || !hyper || (dynamic_scale && growth_interval <= 0)) {
+    cs::set_error("cs_adam_prepare: invalid argument");
+    return CS_EINVAL;
+  }
+  adam_prepare_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_state, *hyper, max_grad_norm, growth_factor, backoff_factor, growth_interval,
+      dynamic_scale);
+  cs::note_launches(1);
+  return launch_error("cs_adam_prepare");
+}

@@ -1,0 +1,147 @@
+// Host fused Adam for optimizer triplets the placement plan keeps in pinned
+// host DRAM (PatrickStar's device-aware placement, PAPER §5;
+// /root/reference/pkg/src/chunkstar/profiler.py:93-130 decides it and
+// engine.py:249-251/265-267 bill the grad D2H and param H2D `adam_copy`).
+//
+// Same per-element arithmetic and rounding as the CUDA kernel K1
+// (cs_adam_chunks): the fmas are explicit _mm256_fmadd_ps, everything else is
+// individually rounded (compiled with -ffp-contract=off), IEEE sqrt/div,
+// round-to-nearest-even narrowing.  8 lanes per step; OpenMP over 64
+// Ki-element ranges of every item.
+#include <immintrin.h>
+#include <omp.h>
+
+#include <cstring>
+#include <vector>
+
+#include "cs_internal.h"
+
+namespace {
+
+struct Consts {
+  __m256 gs, nss, sb, b2, c1, c2, eps, wd, decay;
+  bool adamw, has_wd;
+};
+
+template <int DT>
+__attribute__((target("avx2,fma,f16c"))) inline __m256 load16(const uint16_t* p) {
+  const __m128i h = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p));
+  if (DT == CS_FP16) return _mm256_cvtph_ps(h);
+  return _mm256_castsi256_ps(_mm256_slli_epi32(_mm256_cvtepu16_epi32(h), 16));
+}
+
+template <int DT>
+__attribute__((target("avx2,fma,f16c"))) inline void store16(uint16_t* p, __m256 f) {
+  __m128i h;
+  if (DT == CS_FP16) {
+    h = _mm256_cvtps_ph(f, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+  } else {  // bf16 round-to-nearest-even: (x + 0x7fff + lsb) >> 16
+    const __m256i x = _mm256_castps_si256(f);
+    const __m256i lsb = _mm256_and_si256(_mm256_srli_epi32(x, 16), _mm256_set1_epi32(1));
+    const __m256i r = _mm256_srli_epi32(
+        _mm256_add_epi32(_mm256_add_epi32(x, _mm256_set1_epi32(0x7fff)), lsb), 16);
+    h = _mm_packus_epi32(_mm256_castsi256_si128(r), _mm256_extracti128_si256(r, 1));
+  }
+  _mm_storeu_si128(reinterpret_cast<__m128i*>(p), h);
+}
+
+template <int DT>
+__attribute__((target("avx2,fma,f16c"))) inline void adam8(uint16_t* p16, float* p32, float* m,
+                                                        float* v, const Consts& c) {
+  __m256 g = _mm256_mul_ps(load16<DT>(p16), c.gs);
+  __m256 p = _mm256_loadu_ps(p32);
+  if (c.has_wd) {
+    if (c.adamw) p = _mm256_mul_ps(p, c.decay);
+    else g = _mm256_fmadd_ps(c.wd, p, g);
+  }
+  const __m256 m0 = _mm256_loadu_ps(m);
+  const __m256 mm = _mm256_fmadd_ps(c.c1, _mm256_sub_ps(g, m0), m0);
+  const __m256 vv = _mm256_fmadd_ps(_mm256_mul_ps(c.c2, g), g,
+                                    _mm256_mul_ps(_mm256_loadu_ps(v), c.b2));
+  const __m256 denom = _mm256_add_ps(_mm256_div_ps(_mm256_sqrt_ps(vv), c.sb), c.eps);
+  p = _mm256_add_ps(p, _mm256_div_ps(_mm256_mul_ps(c.nss, mm), denom));
+  _mm256_storeu_ps(p32, p);
+  _mm256_storeu_ps(m, mm);
+  _mm256_storeu_ps(v, vv);
+  store16<DT>(p16, p);
+}
+
+template <int DT>
+__attribute__((target("avx2,fma,f16c"))) void adam_range(const CsAdamItem& it, int64_t lo,
+                                                      int64_t hi, const Consts& c) {
+  uint16_t* p16 = static_cast<uint16_t*>(it.p16);
+  int64_t e = lo;
+  for (; e + 8 <= hi; e += 8) adam8<DT>(p16 + e, it.p32 + e, it.m + e, it.v + e, c);
+  if (e < hi) {  // tail: run the same 8-lane code on a padded copy
+    alignas(32) uint16_t t16[8] = {0};
+    alignas(32) float tp[8] = {0}, tm[8] = {0}, tv[8] = {0};
+    const int64_t k = hi - e;
+    std::memcpy(t16, p16 + e, k * 2);
+    std::memcpy(tp, it.p32 + e, k * 4);
+    std::memcpy(tm, it.m + e, k * 4);
+    std::memcpy(tv, it.v + e, k * 4);
+    adam8<DT>(t16, tp, tm, tv, c);
+    std::memcpy(p16 + e, t16, k * 2);
+    std::memcpy(it.p32 + e, tp, k * 4);
+    std::memcpy(it.m + e, tm, k * 4);
+    std::memcpy(it.v + e, tv, k * 4);
+  }
+}
+
+__attribute__((target("avx2,fma,f16c"))) Consts make_consts(const CsAdamHyper& h,
+                                                         const CsStepState& s) {
+  // scalars formed in double and rounded once, exactly as cs_adam_chunks
+  Consts c;
+  c.gs = _mm256_set1_ps(s.grad_scale);
+  c.nss = _mm256_set1_ps(-s.step_size);
+  c.sb = _mm256_set1_ps(s.sqrt_bc2);
+  c.b2 = _mm256_set1_ps((float)h.beta2);
+  c.c1 = _mm256_set1_ps((float)(1.0 - h.beta1));
+  c.c2 = _mm256_set1_ps((float)(1.0 - h.beta2));
+  c.eps = _mm256_set1_ps((float)h.eps);
+  c.wd = _mm256_set1_ps((float)h.weight_decay);
+  c.decay = _mm256_set1_ps((float)(1.0 - h.lr * h.weight_decay));
+  c.adamw = h.adamw != 0;
+  c.has_wd = h.weight_decay != 0.0f;
+  return c;
+}
+
+}  // namespace
+
+extern "C" int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
+                                   const CsAdamHyper* hyper, const CsStepState* state,
+                                   int n_threads) {
+  if (n_items < 0 || (n_items > 0 && !items) || !hyper || !state ||
+      (dtype != CS_FP16 && dtype != CS_BF16)) {
+    cs::set_error("cs_adam_chunks_host: invalid argument");
+    return CS_EINVAL;
+  }
+  if (!__builtin_cpu_supports("avx2") || !__builtin_cpu_supports("fma") ||
+      !__builtin_cpu_supports("f16c")) {
+    cs::set_error("cs_adam_chunks_host: host CPU lacks AVX2/FMA/F16C");
+    return CS_EINVAL;
+  }
+  if (state->skip) return 0;
+  const Consts c = make_consts(*hyper, *state);
+  constexpr int64_t kRange = 1 << 16;
+  std::vector<std::pair<int, int64_t>> ranges;
+  for (int i = 0; i < n_items; ++i) {
+    if (items[i].n < 0 || (items[i].n > 0 && (!items[i].p16 || !items[i].p32 ||
+                                              !items[i].m || !items[i].v))) {
+      cs::set_error("cs_adam_chunks_host: item %d invalid", i);
+      return CS_EINVAL;
+    }
+    for (int64_t lo = 0; lo < items[i].n; lo += kRange) ranges.emplace_back(i, lo);
+  }
+  const int64_t nr = (int64_t)ranges.size();
+  const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+#pragma omp parallel for num_threads(threads) schedule(static)
+  for (int64_t r = 0; r < nr; ++r) {
+    const CsAdamItem& it = items[ranges[r].first];
+    const int64_t lo = ranges[r].second;
+    const int64_t hi = lo + kRange < it.n ? lo + kRange : it.n;
+    if (dtype == CS_FP16) adam_range<CS_FP16>(it, lo, hi, c);
+    else adam_range<CS_BF16>(it, lo, hi, c);
+  }
+  return 0;
+}

@@ -1,0 +1,207 @@
+"""Tensor-level wrappers over the C ABI (device pointers + the current stream).
+
+Each wrapper takes torch tensors that live on the GPU (or, for
+:func:`adam_chunks_host`, in pinned host memory), extracts raw pointers and
+calls the corresponding ``cs_*`` entry point on the given/current CUDA
+stream.  They validate dtypes and devices and raise on any error: there is
+no CPU path for GPU-resident work.
+"""
+
+import ctypes
+from typing import Iterable, List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _native as N
+
+DTYPE_CODE = {torch.float16: N.CS_FP16, torch.bfloat16: N.CS_BF16}
+SRC_CODE = {torch.float16: N.CS_FP16, torch.bfloat16: N.CS_BF16, torch.float32: N.CS_FP32}
+
+
+def _code(dtype: torch.dtype) -> int:
+    if dtype not in DTYPE_CODE:
+        raise TypeError("chunk payload dtype must be float16 or bfloat16, got %s" % dtype)
+    return DTYPE_CODE[dtype]
+
+
+def _stream(stream: Optional[torch.cuda.Stream]) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*tensors: torch.Tensor) -> None:
+    for t in tensors:
+        if not t.is_cuda:
+            raise ValueError("expected a CUDA tensor, got one on %s" % t.device)
+
+
+class AdamHyper:
+    def __init__(self, lr: float = 1e-4, betas: Tuple[float, float] = (0.9, 0.999),
+                 eps: float = 1e-8, weight_decay: float = 0.0, adamw: bool = False):
+        self.lr, self.betas, self.eps = lr, betas, eps
+        self.weight_decay, self.adamw = weight_decay, adamw
+
+    def c(self) -> N.CsAdamHyper:
+        return N.CsAdamHyper(self.lr, self.betas[0], self.betas[1], self.eps,
+                             self.weight_decay, int(self.adamw))
+
+
+class StepState:
+    """Device-resident ``CsStepState`` (one per optimizer)."""
+
+    NBYTES = 64
+
+    def __init__(self, device: torch.device, init_loss_scale: float = 1.0,
+                 stream: Optional[torch.cuda.Stream] = None):
+        assert ctypes.sizeof(N.CsStepState) <= self.NBYTES
+        self.buf = torch.zeros(self.NBYTES, dtype=torch.uint8, device=device)
+        N.check(N.load().cs_step_state_init(ctypes.c_void_p(self.buf.data_ptr()),
+                                            float(init_loss_scale), _stream(stream)),
+                "cs_step_state_init")
+
+    @property
+    def ptr(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p(self.buf.data_ptr())
+
+    def _f32(self, field: str) -> torch.Tensor:
+        off = getattr(N.CsStepState, field).offset
+        return self.buf[off:off + 4].view(torch.float32)
+
+    def loss_scale(self) -> torch.Tensor:
+        """0-dim device view of the current loss scale (no sync)."""
+        return self._f32("loss_scale")[0]
+
+    def grad_norm(self) -> torch.Tensor:
+        return self._f32("grad_norm")[0]
+
+    def sumsq(self) -> torch.Tensor:
+        return self._f32("sumsq")
+
+    def read(self) -> N.CsStepState:
+        """Host copy (synchronises the buffer's stream)."""
+        raw = bytes(self.buf.cpu().numpy().tobytes())
+        return N.CsStepState.from_buffer_copy(raw[:ctypes.sizeof(N.CsStepState)])
+
+
+def adam_chunks(items: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, int]],
+                hyper: AdamHyper, state: StepState,
+                stream: Optional[torch.cuda.Stream] = None) -> None:
+    """K1 over many (p16, p32, m, v, n) items in one launch (per 256 items)."""
+    if not items:
+        return
+    arr = (N.CsAdamItem * len(items))()
+    dt = _code(items[0][0].dtype)
+    for i, (p16, p32, m, v, n) in enumerate(items):
+        _need_cuda(p16, p32, m, v)
+        if p16.dtype != items[0][0].dtype or p32.dtype != torch.float32:
+            raise TypeError("mixed or wrong dtypes in adam items")
+        if min(p16.numel(), p32.numel(), m.numel(), v.numel()) < n:
+            raise ValueError("adam item %d: n=%d exceeds a buffer" % (i, n))
+        arr[i] = N.CsAdamItem(p16.data_ptr(), p32.data_ptr(), m.data_ptr(), v.data_ptr(), n)
+    h = hyper.c()
+    N.check(N.load().cs_adam_chunks(arr, len(items), dt, ctypes.byref(h), state.ptr,
+                                    _stream(stream)), "cs_adam_chunks")
+
+
+def adam_chunks_host(items, hyper: AdamHyper, state: N.CsStepState, n_threads: int = 0) -> None:
+    """Host Adam for CPU-placed positions (tensors in host memory)."""
+    if not items:
+        return
+    arr = (N.CsAdamItem * len(items))()
+    dt = _code(items[0][0].dtype)
+    for i, (p16, p32, m, v, n) in enumerate(items):
+        if p16.is_cuda or p32.is_cuda:
+            raise ValueError("host adam needs host tensors")
+        arr[i] = N.CsAdamItem(p16.data_ptr(), p32.data_ptr(), m.data_ptr(), v.data_ptr(), n)
+    h = hyper.c()
+    N.check(N.load().cs_adam_chunks_host(arr, len(items), dt, ctypes.byref(h),
+                                         ctypes.byref(state), int(n_threads)),
+            "cs_adam_chunks_host")
+
+
+def sumsq_partials() -> int:
+    n = N.load().cs_sumsq_partials()
+    if n <= 0:
+        raise N.NativeError("cs_sumsq_partials: no device")
+    return n
+
+
+def grad_sumsq(grads: Sequence[Tuple[torch.Tensor, int]], partials: torch.Tensor,
+               stream: Optional[torch.cuda.Stream] = None,
+               dtype: Optional[torch.dtype] = None) -> None:
+    """K2: per-block partial sums of squares of the given gradient prefixes."""
+    arr = (N.CsGradItem * max(len(grads), 1))()
+    for i, (g, n) in enumerate(grads):
+        _need_cuda(g)
+        arr[i] = N.CsGradItem(g.data_ptr(), n)
+    dt = _code(dtype if dtype is not None else grads[0][0].dtype)
+    N.check(N.load().cs_grad_sumsq(arr, len(grads), dt, ctypes.c_void_p(partials.data_ptr()),
+                                   _stream(stream)), "cs_grad_sumsq")
+
+
+def sumsq_finalize(partials: torch.Tensor, state: StepState, accumulate: bool = False,
+                   stream: Optional[torch.cuda.Stream] = None) -> None:
+    N.check(N.load().cs_sumsq_finalize(ctypes.c_void_p(partials.data_ptr()), partials.numel(),
+                                       state.ptr, int(accumulate), _stream(stream)),
+            "cs_sumsq_finalize")
+
+
+def adam_prepare(state: StepState, hyper: AdamHyper, max_grad_norm: float = 0.0,
+                 growth_factor: float = 2.0, backoff_factor: float = 0.5,
+                 growth_interval: int = 2000, dynamic_scale: bool = False,
+                 stream: Optional[torch.cuda.Stream] = None) -> None:
+    h = hyper.c()
+    N.check(N.load().cs_adam_prepare(state.ptr, ctypes.byref(h), float(max_grad_norm),
+                                     float(growth_factor), float(backoff_factor),
+                                     int(growth_interval), int(dynamic_scale),
+                                     _stream(stream)), "cs_adam_prepare")
+
+
+def _pack_items(items) -> "ctypes.Array":
+    arr = (N.CsPackItem * len(items))()
+    for i, (chunk, offset, src, n) in enumerate(items):
+        _need_cuda(chunk, src)
+        if offset < 0 or offset + n > chunk.numel() or n > src.numel():
+            raise ValueError("pack item %d out of bounds" % i)
+        arr[i] = N.CsPackItem(chunk.data_ptr(), offset, src.data_ptr(), n)
+    return arr
+
+
+def pack(items: Sequence[Tuple[torch.Tensor, int, torch.Tensor, int]], accumulate: bool = False,
+         stream: Optional[torch.cuda.Stream] = None) -> None:
+    """K3 (slot = src) / K4 (slot += src) over (chunk, offset, src, n) items."""
+    if not items:
+        return
+    dt = _code(items[0][0].dtype)
+    for chunk, _, src, _ in items:
+        if chunk.dtype != src.dtype:
+            raise TypeError("pack: chunk and source dtypes differ")
+    N.check(N.load().cs_pack(_pack_items(items), len(items), dt, int(accumulate),
+                             _stream(stream)), "cs_pack")
+
+
+def cast_pack(items: Sequence[Tuple[torch.Tensor, int, torch.Tensor, int]],
+              stream: Optional[torch.cuda.Stream] = None) -> None:
+    """K5: fp32 sources -> fp16/bf16 chunk slots."""
+    if not items:
+        return
+    dt = _code(items[0][0].dtype)
+    for _, _, src, _ in items:
+        if src.dtype != torch.float32:
+            raise TypeError("cast_pack sources must be float32")
+    N.check(N.load().cs_cast_pack(_pack_items(items), len(items), dt, _stream(stream)),
+            "cs_cast_pack")
+
+
+def master_init(p32: torch.Tensor, m: torch.Tensor, v: torch.Tensor, src: torch.Tensor,
+                n: int, stream: Optional[torch.cuda.Stream] = None) -> None:
+    """K6: p32 = float(src[:n]), m = v = 0.  ``src`` may be pinned host memory."""
+    _need_cuda(p32, m, v)
+    if src.dtype not in SRC_CODE:
+        raise TypeError("master_init source dtype %s" % src.dtype)
+    if not src.is_cuda and not src.is_pinned():
+        raise ValueError("master_init host source must be pinned (device-mapped)")
+    N.check(N.load().cs_master_init(ctypes.c_void_p(p32.data_ptr()), ctypes.c_void_p(m.data_ptr()),
+                                    ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(src.data_ptr()),
+                                    SRC_CODE[src.dtype], int(n), _stream(stream)),
+            "cs_master_init")

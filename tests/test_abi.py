@@ -1,0 +1,72 @@
+"""The C-ABI library builds for sm_100a, loads and exports the header's API.
+
+No GPU needed: only symbol resolution, struct layout and argument errors.
+"""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "chunkstar_b200.h")
+
+
+def _declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(cs_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_expected_entry_points():
+    names = _declared_functions()
+    for must in ("cs_adam_chunks", "cs_grad_sumsq", "cs_pack", "cs_cast_pack",
+                 "cs_master_init", "cs_adam_prepare", "cs_adam_chunks_host"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(native_lib):
+    from paper_2108_05818_b200 import _native
+    for name in _declared_functions():
+        assert hasattr(native_lib, name), name
+        assert name in _native.SIGNATURES, "binding missing for %s" % name
+
+
+def test_library_targets_sm100a():
+    from paper_2108_05818_b200 import _native
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_struct_layouts_match_header(tmp_path, native_lib):
+    from paper_2108_05818_b200 import _native as N
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "chunkstar_b200.h"\n'
+                   'int main(void){\n'
+                   ' printf("%zu %zu %zu %zu %zu\\n", sizeof(CsAdamHyper), sizeof(CsStepState),'
+                   ' sizeof(CsAdamItem), sizeof(CsGradItem), sizeof(CsPackItem));\n'
+                   ' printf("%zu %zu %zu %zu\\n", offsetof(CsStepState, loss_scale),'
+                   ' offsetof(CsStepState, grad_scale), offsetof(CsStepState, skip),'
+                   ' offsetof(CsStepState, sumsq));\n return 0; }\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                   check=True)
+    sizes, offs = subprocess.run([str(exe)], capture_output=True, text=True).stdout.split("\n")[:2]
+    assert [int(x) for x in sizes.split()] == [
+        ctypes.sizeof(N.CsAdamHyper), ctypes.sizeof(N.CsStepState), ctypes.sizeof(N.CsAdamItem),
+        ctypes.sizeof(N.CsGradItem), ctypes.sizeof(N.CsPackItem)]
+    assert [int(x) for x in offs.split()] == [
+        N.CsStepState.loss_scale.offset, N.CsStepState.grad_scale.offset,
+        N.CsStepState.skip.offset, N.CsStepState.sumsq.offset]
+    assert ctypes.sizeof(N.CsStepState) <= 64
+
+
+def test_argument_errors_are_reported(native_lib):
+    from paper_2108_05818_b200 import _native as N
+    rc = native_lib.cs_pack(None, -1, N.CS_FP16, 0, None)
+    assert rc == -1 and b"invalid" in native_lib.cs_last_error()
+    rc = native_lib.cs_master_init(None, None, None, None, 7, 4, None)
+    assert rc == -1
+    assert native_lib.cs_version().startswith(b"chunkstar_b200")

@@ -1,0 +1,197 @@
+"""GPU parity of the sm_100a chunk kernels vs the C oracle (bit-exact).
+
+K1 fused chunk Adam, K2 grad sum-of-squares (+ deterministic finalize and
+the device-side step scalars), K3 pack, K4 accumulate, K5 cast+pack, K6
+optimizer-state birth.  Inputs are seeded; sizes cover tails (n % 4, n % 8),
+multi-item launches (> 256 items → several launches), unaligned slot
+offsets, fp16 and bf16, L2 and decoupled weight decay, and the skip path.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA GPU")]
+
+from paper_2108_05818_b200 import kernels as K  # noqa: E402
+
+DEV = "cuda"
+
+
+def _bits16(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().view(torch.int16).numpy().view(np.uint16).copy()
+
+
+def _code(O, dtype):
+    return O.FP16 if dtype == torch.float16 else O.BF16
+
+
+def _oracle_state(O, st: "K.N.CsStepState"):
+    s = O.OrStepState()
+    for f, _ in s._fields_:
+        setattr(s, f, getattr(st, f))
+    return s
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("wd,adamw", [(0.0, False), (0.1, False), (0.01, True)])
+def test_adam_chunks_bit_exact(native_lib, oracle_lib, dtype, wd, adamw):
+    O = oracle_lib
+    g = torch.Generator(device="cpu").manual_seed(11)
+    sizes = [1, 3, 4, 5, 4095, 4096, 4097, 70001, (1 << 20) + 7]
+    hyper = K.AdamHyper(lr=3e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=wd, adamw=adamw)
+    state = K.StepState(DEV, init_loss_scale=4.0)
+    state.sumsq().fill_(5.0)
+    K.adam_prepare(state, hyper)
+    host_state = state.read()
+    items, ref = [], []
+    for n in sizes:
+        gr = (torch.randn(n, generator=g) * 1e-2).to(dtype)
+        p = torch.randn(n, generator=g) * 0.02
+        m = torch.randn(n, generator=g) * 1e-3
+        v = torch.rand(n, generator=g) * 1e-5
+        ref.append([_bits16(gr), p.numpy().copy(), m.numpy().copy(), v.numpy().copy()])
+        items.append((gr.to(DEV), p.to(DEV), m.to(DEV), v.to(DEV), n))
+    K.adam_chunks(items, hyper, state)
+    torch.cuda.synchronize()
+    s = _oracle_state(O, host_state)
+    for (gr, p, m, v, n), (rg, rp, rm, rv) in zip(items, ref):
+        O.adam(rg, rp, rm, rv, n, _code(O, dtype), 3e-4, 0.9, 0.999, 1e-8, wd, adamw, s)
+        np.testing.assert_array_equal(p.cpu().numpy().view(np.uint32), rp.view(np.uint32))
+        np.testing.assert_array_equal(m.cpu().numpy().view(np.uint32), rm.view(np.uint32))
+        np.testing.assert_array_equal(v.cpu().numpy().view(np.uint32), rv.view(np.uint32))
+        np.testing.assert_array_equal(_bits16(gr), rg)
+
+
+def test_adam_chunks_many_items_and_prefix_only(native_lib, oracle_lib):
+    """300 items (two launches); only the used prefix of each chunk changes."""
+    O = oracle_lib
+    cap, used = 8192, 5000
+    hyper = K.AdamHyper(lr=1e-3)
+    state = K.StepState(DEV)
+    state.sumsq().fill_(1.0)
+    K.adam_prepare(state, hyper)
+    s = _oracle_state(O, state.read())
+    chunks = []
+    for i in range(300):
+        gen = torch.Generator().manual_seed(i)
+        p16 = (torch.randn(cap, generator=gen) * 1e-3).half()
+        p32 = torch.randn(cap, generator=gen) * 0.02
+        m = torch.zeros(cap)
+        v = torch.zeros(cap)
+        chunks.append([x.to(DEV) for x in (p16, p32, m, v)] + [x.numpy().copy() for x in (p32, m, v)]
+                      + [_bits16(p16)])
+    K.adam_chunks([(c[0], c[1], c[2], c[3], used) for c in chunks], hyper, state)
+    torch.cuda.synchronize()
+    for c in chunks:
+        rp, rm, rv, rg = c[4], c[5], c[6], c[7]
+        tail = rg[used:].copy(), rp[used:].copy()
+        O.adam(rg, rp, rm, rv, used, O.FP16, 1e-3, 0.9, 0.999, 1e-8, 0.0, False, s)
+        np.testing.assert_array_equal(c[1].cpu().numpy().view(np.uint32), rp.view(np.uint32))
+        np.testing.assert_array_equal(_bits16(c[0]), rg)
+        np.testing.assert_array_equal(_bits16(c[0])[used:], tail[0])
+
+
+def test_adam_skip_leaves_state_untouched(native_lib):
+    hyper = K.AdamHyper()
+    state = K.StepState(DEV, init_loss_scale=65536.0)
+    state.sumsq().fill_(float("inf"))
+    K.adam_prepare(state, hyper, dynamic_scale=True)
+    st = state.read()
+    assert st.skip == 1 and st.step == 0 and st.loss_scale == 32768.0
+    p16 = torch.full((1000,), float("inf"), dtype=torch.float16, device=DEV)
+    p32 = torch.ones(1000, device=DEV)
+    m = torch.zeros(1000, device=DEV)
+    v = torch.zeros(1000, device=DEV)
+    K.adam_chunks([(p16, p32, m, v, 1000)], hyper, state)
+    torch.cuda.synchronize()
+    assert (p32 == 1).all() and (m == 0).all() and torch.isinf(p16).all()
+
+
+def test_grad_sumsq_and_step_scalars_match_oracle(native_lib, oracle_lib):
+    O = oracle_lib
+    gen = torch.Generator().manual_seed(5)
+    grads = [(torch.randn(n, generator=gen) * 3).half() for n in (1, 4097, 300000, 1 << 21)]
+    partials = torch.empty(K.sumsq_partials(), device=DEV)
+    state = K.StepState(DEV, init_loss_scale=2.0)
+    K.grad_sumsq([(x.to(DEV), x.numel()) for x in grads], partials)
+    K.sumsq_finalize(partials, state)
+    hyper = K.AdamHyper(lr=1e-3, betas=(0.9, 0.99))
+    K.adam_prepare(state, hyper, max_grad_norm=1.0, dynamic_scale=True, growth_interval=1)
+    st = state.read()
+    ref = sum(O.grad_sumsq(_bits16(x), O.FP16) for x in grads)
+    assert abs(st.sumsq - ref) <= 1e-5 * ref
+    s = O.step_state(2.0)
+    s.sumsq = st.sumsq  # same input -> identical scalars
+    O.adam_prepare(s, 1e-3, 0.9, 0.99, max_norm=1.0, dynamic=True, interval=1)
+    for f in ("grad_scale", "step_size", "sqrt_bc2", "grad_norm", "loss_scale", "step", "skip",
+              "beta1_pow", "beta2_pow"):
+        assert getattr(st, f) == getattr(s, f), f
+    # determinism: same inputs, same partials, bit-identical sumsq
+    K.grad_sumsq([(x.to(DEV), x.numel()) for x in grads], partials)
+    K.sumsq_finalize(partials, state)
+    assert state.read().sumsq == st.sumsq
+
+
+def test_grad_sumsq_detects_inf(native_lib):
+    g = torch.randn(10000, device=DEV).half()
+    g[1234] = float("inf")
+    partials = torch.empty(K.sumsq_partials(), device=DEV)
+    state = K.StepState(DEV)
+    K.grad_sumsq([(g, g.numel())], partials)
+    K.sumsq_finalize(partials, state)
+    assert not np.isfinite(state.read().sumsq)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_pack_and_accumulate_bit_exact(native_lib, oracle_lib, dtype, accumulate):
+    O = oracle_lib
+    gen = torch.Generator().manual_seed(2)
+    cap = 200003
+    chunk = (torch.randn(cap, generator=gen)).to(dtype)
+    # aligned, unaligned and tail-heavy slots (gap-free packing offsets)
+    slots = [(0, 65536), (65536, 131072 - 65536 + 5), (131077, 3), (131080, 68923)]
+    srcs = [(torch.randn(n, generator=gen)).to(dtype) for _, n in slots]
+    ref = _bits16(chunk)
+    for (off, n), s in zip(slots, srcs):
+        O.pack(ref, off, _bits16(s), _code(O, dtype), accumulate)
+    dchunk = chunk.to(DEV)
+    K.pack([(dchunk, off, s.to(DEV), n) for (off, n), s in zip(slots, srcs)], accumulate=accumulate)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits16(dchunk), ref)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_cast_pack_bit_exact(native_lib, oracle_lib, dtype):
+    O = oracle_lib
+    gen = torch.Generator().manual_seed(4)
+    cap = 100000
+    chunk = torch.zeros(cap, dtype=dtype)
+    slots = [(0, 4096), (4096, 12345), (16441, 7), (16448, 83552)]
+    srcs = [torch.randn(n, generator=gen) * 0.02 for _, n in slots]
+    ref = _bits16(chunk)
+    for (off, n), s in zip(slots, srcs):
+        O.cast_pack(ref, off, s.numpy().copy(), _code(O, dtype))
+    dchunk = chunk.to(DEV)
+    K.cast_pack([(dchunk, off, s.to(DEV), n) for (off, n), s in zip(slots, srcs)])
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(_bits16(dchunk), ref)
+    # and the GPU cast equals torch's own RN cast
+    np.testing.assert_array_equal(_bits16(dchunk[:4096].cpu()), _bits16(srcs[0].to(dtype)))
+
+
+@pytest.mark.parametrize("src_dtype", [torch.float16, torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("pinned_host", [False, True])
+def test_master_init(native_lib, src_dtype, pinned_host):
+    n = 70001
+    src = (torch.randn(n) * 0.02).to(src_dtype)
+    src = src.pin_memory() if pinned_host else src.to(DEV)
+    p32 = torch.full((n,), 7.0, device=DEV)
+    m = torch.full((n,), 7.0, device=DEV)
+    v = torch.full((n,), 7.0, device=DEV)
+    K.master_init(p32, m, v, src, n)
+    torch.cuda.synchronize()
+    assert torch.equal(p32.cpu(), src.cpu().float())
+    assert (m == 0).all() and (v == 0).all()
