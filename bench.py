@@ -1,0 +1,309 @@
+"""Benchmark of the chunk-managed GPT training step (PatrickStar) on B200.
+
+Workload (BASELINE.json configs[1]): GPT-2 1B (L20 H2048, 16 heads,
+S1024, V50304), fp16 chunks with dynamic loss scaling, all chunks
+HBM-resident, per-GPU batch --batch (default 16), chunk capacity --cap
+(default 64Mi elements).  A step = warm-up-planned chunk-managed forward +
+backward + fused chunk Adam over one synthetic batch per GPU; N>1 ranks run
+ZeRO chunk groups over NCCL (weak scaling: fixed per-GPU batch).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl chunk|reference]
+
+Prints one JSON line (rank 0).  ``value`` = tokens/s over all ranks with
+inputs already in HBM (CUDA events, max over ranks); ``e2e`` = the same
+through ChunkTrainer.step_host (pinned host tokens H2D + loss D2H inside the
+timed region).  ``roofline`` = K1 fused chunk Adam timed in-region with
+CUDA events on the compute stream.  ``cpu_baseline`` = the CPU port of the
+step (oracle/cpu_step.py) on a bounded sample, rank 0 at N=1 only.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPT tokens/sec & TFLOPS/GPU at 1/2/4/8 B200; chunk-Adam HBM GB/s vs peak"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="chunk", choices=["chunk", "reference"])
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--cap", type=int, default=64 << 20)
+    ap.add_argument("--layers", type=int, default=20)
+    ap.add_argument("--hidden", type=int, default=2048)
+    ap.add_argument("--heads", type=int, default=16)
+    ap.add_argument("--seq", type=int, default=1024)
+    ap.add_argument("--vocab", type=int, default=50304)
+    ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-batch", type=int, default=1)
+    return ap.parse_args()
+
+
+def model_flops_per_step(B, S, L, H, V):
+    """72·B·S·L·H²·(1 + S/(6H) + V/(12·L·H)) per GPU-batch."""
+    return 72.0 * B * S * L * H * H * (1 + S / (6.0 * H) + V / (12.0 * L * H))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", 1382.7)), "measured"
+    except Exception:
+        return 6650.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(schema_kw, sample_batch, steps=1):
+    from oracle.cpu_step import CpuChunkStep
+    from paper_2108_05818_b200.model import build_gpt_schema
+    schema = build_gpt_schema(**schema_kw)
+    runner = CpuChunkStep(schema, sample_batch=sample_batch)
+    secs = [runner.step() for _ in range(steps)]
+    t = min(secs)
+    return {"value": round(runner.tokens_per_step / t, 3), "unit": UNIT,
+            "cores": runner.threads, "kind": "port",
+            "sample": "%d x %d tokens on the full %d-layer H%d model per step (fp32 torch-CPU "
+                      "fwd/bwd + C-oracle chunk Adam over all %.2fB params + the decision "
+                      "engine), best of %d" % (sample_batch, schema.seq_len, schema.layers,
+                                               schema.hidden_dim,
+                                               sum(p.numel() for p in runner.model.parameters())
+                                               / 1e9, steps)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    schema_kw = dict(layers=args.layers, hidden_dim=args.hidden, heads=args.heads,
+                     seq_len=args.seq, vocab=args.vocab, batch=args.batch)
+    from oracle.cpu_step import CpuChunkStep
+    from paper_2108_05818_b200.model import build_gpt_schema
+    runner = CpuChunkStep(build_gpt_schema(**schema_kw), sample_batch=args.cpu_sample_batch)
+    for _ in range(args.warmup):
+        runner.step()
+    secs = [runner.step() for _ in range(args.steps)]
+    total = sum(secs)
+    value = runner.tokens_per_step * len(secs) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / len(secs), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": "GPT 1B chunk-managed training step (reference CPU path, "
+                               "bounded sample)", "model": "GPT L%d H%d" % (args.layers,
+                                                                             args.hidden),
+                   "per_step_sample_tokens": runner.tokens_per_step},
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": runner.threads,
+                         "kind": "port",
+                         "sample": "%d x %d tokens per step on the full model"
+                                   % (args.cpu_sample_batch, args.seq)},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2108_05818_b200 import _native
+    from paper_2108_05818_b200 import kernels as K
+    from paper_2108_05818_b200.config import PolicySpec
+    from paper_2108_05818_b200.model import build_gpt_schema
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    schema_kw = dict(layers=args.layers, hidden_dim=args.hidden, heads=args.heads,
+                     seq_len=args.seq, vocab=args.vocab, batch=args.batch)
+    schema = build_gpt_schema(**schema_kw)
+    dtype = torch.float16 if args.dtype == "fp16" else torch.bfloat16
+    trainer = ChunkTrainer(schema, PolicySpec(capacity_elems=args.cap), dtype=dtype, seed=0,
+                           hyper=K.AdamHyper(lr=1e-4, betas=(0.9, 0.999), eps=1e-8))
+    ex = trainer.executor
+    B, S = args.batch, args.seq
+    gen = torch.Generator().manual_seed(1000 + rank)
+    pool = [torch.randint(0, args.vocab, (B, S + 1), generator=gen).pin_memory()
+            for _ in range(4)]
+    dev_pool = [t.to(dev) for t in pool]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for i in range(max(args.warmup, 1)):
+        trainer.step(dev_pool[i % 4])
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region 1: device-resident inputs -> value -----------------------
+    ex.record_k1 = True
+    ex.k1_events.clear()
+    launches0 = _native.launch_count()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for k in range(args.steps):
+        loss = trainer.step(dev_pool[k % 4])
+    t1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = _native.launch_count() - launches0
+    ms = t0.elapsed_time(t1) / args.steps
+    ex.record_k1 = False
+    k1_ms = [a.elapsed_time(b) for a, b, _ in ex.k1_events]
+    k1_elems = [n for _, _, n in ex.k1_events]
+    final_loss = float(loss.item())
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+
+    # ---- timed region 2: end to end through the public API -----------------------
+    torch.cuda.synchronize()
+    barrier()
+    e0 = time.perf_counter()
+    for k in range(args.steps):
+        trainer.step_host(pool[k % 4])
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - e0) * 1e3 / args.steps
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    hbm_peak, bf16_peak, peak_src = measured_peaks()
+    tokens_per_step = world * B * S
+    flops = model_flops_per_step(B, S, args.layers, args.hidden, args.vocab)
+    k1_avg_ms = sum(k1_ms) / len(k1_ms) if k1_ms else float("nan")
+    k1_bytes = 28.0 * (sum(k1_elems) / len(k1_elems)) if k1_elems else 0.0
+    k1_gbs = k1_bytes / (k1_avg_ms * 1e-3) / 1e9 if k1_ms else None
+    st = trainer.step_state()
+    out = {
+        "metric": METRIC, "value": round(tokens_per_step / (ms * 1e-3), 1), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": "GPT-2 1B chunk-managed training step (configs[1])",
+                   "model": "GPT L%d H%d heads%d S%d V%d (reference-shaped, 8 chunked "
+                            "tensors/layer)" % (args.layers, args.hidden, args.heads, S,
+                                                args.vocab),
+                   "global_batch": world * B, "per_gpu_batch": B, "seq_len": S,
+                   "chunk_capacity_elems": args.cap,
+                   "positions": trainer.sim.chunk_set.positions,
+                   "parallelism": "zero-chunk-dp%d" % world,
+                   "os_on_gpu": len(trainer.sim.engine.plan.os_positions_on_gpu),
+                   "l2": "inputs larger than L2 (16 GB of chunk state streamed per step)"},
+        "tflops_per_gpu": round(flops / (ms * 1e-3) / 1e12, 2),
+        "tflops_frac_of_sustained_bf16": round(flops / (ms * 1e-3) / 1e12 / bf16_peak, 4),
+        "roofline": {"kernel": "cs_adam_chunks (K1 fused chunk Adam)", "bound": "hbm",
+                     "achieved": round(k1_gbs, 1) if k1_gbs else None, "peak": hbm_peak,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(k1_gbs / hbm_peak, 4) if k1_gbs else None,
+                     "traffic": None,
+                     "algorithmic_bytes_per_launch": k1_bytes,
+                     "elements_per_launch": int(k1_bytes // 28),
+                     "avg_launch_ms": round(k1_avg_ms, 4),
+                     "share_of_step": round(k1_avg_ms / ms, 4)},
+        "e2e": {"value": round(tokens_per_step / (e2e_ms * 1e-3), 1), "unit": UNIT,
+                "h2d_bytes_per_step": pool[0].numel() * pool[0].element_size(),
+                "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "final_loss": final_loss, "loss_scale": st.loss_scale, "adam_steps": int(st.step),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline(schema_kw, args.cpu_sample_batch)
+        except Exception as e:  # reported, never fatal
+            out["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

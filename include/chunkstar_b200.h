@@ -170,6 +170,12 @@ int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
                         const CsAdamHyper* hyper, const CsStepState* state,
                         int n_threads);
 
+/* Host sum of squares (double accumulation) of fp16/bf16 gradients that sit
+ * in host DRAM (grads of a chunk evicted to the CPU before the ADAM event,
+ * or of CPU-placed positions); contributes to CsStepState.sumsq. */
+int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtype, double* out,
+                       int n_threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,8 @@ SIGNATURES = {
     "cs_adam_chunks_host": (ctypes.c_int, [ctypes.POINTER(CsAdamItem), ctypes.c_int,
                                            ctypes.c_int, ctypes.POINTER(CsAdamHyper),
                                            ctypes.POINTER(CsStepState), ctypes.c_int]),
+    "cs_grad_sumsq_host": (ctypes.c_int, [ctypes.POINTER(CsGradItem), ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_double), ctypes.c_int]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

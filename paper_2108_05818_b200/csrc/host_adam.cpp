@@ -145,3 +145,48 @@ extern "C" int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dty
   }
   return 0;
 }
+
+namespace {
+template <int DT>
+__attribute__((target("avx2,f16c"))) double sumsq_range(const uint16_t* g, int64_t n,
+                                                        int threads) {
+  double acc = 0.0;
+#pragma omp parallel for num_threads(threads) reduction(+ : acc) schedule(static)
+  for (int64_t e = 0; e < n; ++e) {
+    float f;
+    if (DT == CS_FP16) {
+      f = _cvtsh_ss(g[e]);
+    } else {
+      const uint32_t u = (uint32_t)g[e] << 16;
+      std::memcpy(&f, &u, 4);
+    }
+    acc += (double)f * (double)f;
+  }
+  return acc;
+}
+}  // namespace
+
+extern "C" int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtype, double* out,
+                                  int n_threads) {
+  if (n_items < 0 || (n_items > 0 && !items) || !out || (dtype != CS_FP16 && dtype != CS_BF16)) {
+    cs::set_error("cs_grad_sumsq_host: invalid argument");
+    return CS_EINVAL;
+  }
+  if (!__builtin_cpu_supports("avx2") || !__builtin_cpu_supports("f16c")) {
+    cs::set_error("cs_grad_sumsq_host: host CPU lacks AVX2/F16C");
+    return CS_EINVAL;
+  }
+  const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+  double total = 0.0;
+  for (int i = 0; i < n_items; ++i) {
+    const uint16_t* g = static_cast<const uint16_t*>(items[i].g16);
+    if (items[i].n > 0 && !g) {
+      cs::set_error("cs_grad_sumsq_host: item %d invalid", i);
+      return CS_EINVAL;
+    }
+    total += dtype == CS_FP16 ? sumsq_range<CS_FP16>(g, items[i].n, threads)
+                              : sumsq_range<CS_BF16>(g, items[i].n, threads);
+  }
+  *out = total;
+  return 0;
+}

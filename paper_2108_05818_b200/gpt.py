@@ -1,0 +1,243 @@
+"""Reference-shaped GPT whose chunk-managed parameters are exactly
+``param_tensor_specs(schema)`` (`/root/reference/pkg/src/chunkstar/model.py:163-191`).
+
+Per layer, four operator slots:
+
+    qkv      three [H, H] projections           (tensor ids 8l+0..2)
+    attn_out one [H, H] projection              (8l+3)
+    mlp_in   two [2H, H] halves, outputs concat (8l+4, 8l+5)
+    mlp_out  two [H, 2H] halves, outputs summed (8l+6, 8l+7)
+
+No biases and non-affine LayerNorms, so nothing else needs chunk
+management; token/position embeddings (tied LM head) are the reference's
+non-chunked embedding allocation (`chunks.py:204-224`).  Splitting a GEMM
+along N (concat) or K (sum) changes nothing but rounding order.
+
+Each slot is bracketed by two autograd markers so the *real* forward and
+backward drive the engine's events in timeline order (`model.py:263-329`):
+
+* ``_SlotEnter`` on the slot inputs: forward = event start (gather, fetch,
+  bind parameter views); backward = BWD event *finish* (it runs only once
+  every dX of the slot is computed, i.e. after all of its dW were written);
+* ``_SlotExit`` on the slot outputs: forward = FWD event finish; backward =
+  BWD event *start* (before any of the slot's backward GEMMs).
+
+:class:`ChunkLinear` keeps a reference to the ``nn.Parameter`` itself rather
+than a saved view, so a chunk that was evicted and re-fetched (new storage)
+between FWD and BWD is read from its current location; in backward it
+computes dX first and then writes dW *directly into the parameter's chunk
+slot* (``torch.mm(..., out=slot)``) — the gradient-overwrites-parameter
+reuse of PatrickStar §4 with zero extra traffic (the K3 pack kernel is used
+where a gradient arrives from autograd instead, e.g. the embedding).
+"""
+
+from typing import Callable, List, Optional, Sequence, Tuple
+
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from .model import ModelSchema, OP_SLOTS, param_tensor_specs
+
+
+class _ChunkLinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x: torch.Tensor, weight: nn.Parameter, grad_sink: Callable):
+        ctx.weight = weight          # the Parameter object, not a saved view
+        ctx.grad_sink = grad_sink
+        ctx.save_for_backward(x)
+        return F.linear(x, weight)
+
+    @staticmethod
+    def backward(ctx, dy: torch.Tensor):
+        (x,) = ctx.saved_tensors
+        w = ctx.weight
+        dx = dy.matmul(w)            # needs W: computed before the slot is overwritten
+        ctx.grad_sink(w, dy.reshape(-1, dy.shape[-1]), x.reshape(-1, x.shape[-1]))
+        return dx, None, None
+
+
+def write_grad_into_slot(w: nn.Parameter, dy2: torch.Tensor, x2: torch.Tensor) -> None:
+    """dW = dy^T x written over the parameter's own chunk slot."""
+    torch.mm(dy2.t(), x2, out=w.data)
+
+
+class _SlotEnter(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, driver, ev_fwd, ev_bwd, *xs):
+        ctx.driver, ctx.ev_bwd = driver, ev_bwd
+        driver.start(ev_fwd)
+        return tuple(x.view_as(x) for x in xs) if len(xs) > 1 else xs[0].view_as(xs[0])
+
+    @staticmethod
+    def backward(ctx, *grads):
+        ctx.driver.finish(ctx.ev_bwd)
+        return (None, None, None) + grads
+
+
+class _SlotExit(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, driver, ev_fwd, ev_bwd, *ys):
+        ctx.driver, ctx.ev_bwd = driver, ev_bwd
+        driver.finish(ev_fwd)
+        return tuple(y.view_as(y) for y in ys) if len(ys) > 1 else ys[0].view_as(ys[0])
+
+    @staticmethod
+    def backward(ctx, *grads):
+        ctx.driver.start(ctx.ev_bwd)
+        return (None, None, None) + grads
+
+
+class _EmbeddingMark(torch.autograd.Function):
+    """embedding.fwd finishes at the lookup; embedding.bwd is the gradient
+    arriving at the embedding output (after l0.qkv.bwd), start and finish."""
+
+    @staticmethod
+    def forward(ctx, driver, ev_fwd, ev_bwd, h):
+        ctx.driver, ctx.ev_bwd = driver, ev_bwd
+        driver.finish(ev_fwd)
+        return h.view_as(h)
+
+    @staticmethod
+    def backward(ctx, grad):
+        ctx.driver.start(ctx.ev_bwd)
+        ctx.driver.finish(ctx.ev_bwd)
+        return None, None, None, grad
+
+
+class EventDriver:
+    """Forwards marker callbacks to the engine; inert when no engine is attached."""
+
+    def __init__(self):
+        self.on_start: Optional[Callable[[int], None]] = None
+        self.on_finish: Optional[Callable[[int], None]] = None
+
+    def start(self, ev: int) -> None:
+        if self.on_start is not None and ev >= 0:
+            self.on_start(ev)
+
+    def finish(self, ev: int) -> None:
+        if self.on_finish is not None and ev >= 0:
+            self.on_finish(ev)
+
+
+def _bracket(marker, driver, ev_fwd, ev_bwd, xs):
+    out = marker.apply(driver, ev_fwd, ev_bwd, *xs)
+    return out if isinstance(out, tuple) else (out,)
+
+
+class GPTBlock(nn.Module):
+    def __init__(self, schema: ModelSchema, layer: int, driver: EventDriver,
+                 dtype: torch.dtype, grad_sink: Callable, placeholders: bool = False):
+        super().__init__()
+        H = schema.hidden_dim
+        self.heads, self.layer, self.driver, self.grad_sink = schema.heads, layer, driver, grad_sink
+        shapes = {"qkv": [(H, H)] * 3, "attn_out": [(H, H)], "mlp_in": [(2 * H, H)] * 2,
+                  "mlp_out": [(H, 2 * H)] * 2}
+        self.slots = nn.ModuleDict()
+        for name, _ in OP_SLOTS:
+            self.slots[name] = nn.ParameterList(
+                [nn.Parameter(torch.empty(0 if placeholders else s, dtype=dtype),
+                              requires_grad=True)
+                 for s in shapes[name]])
+        # (fwd event index, bwd event index) per slot, filled by attach_events
+        self.events = {name: (-1, -1) for name, _ in OP_SLOTS}
+
+    def _lin(self, x, w):
+        return _ChunkLinearFn.apply(x, w, self.grad_sink)
+
+    def _slot(self, name, xs, fn):
+        fwd, bwd = self.events[name]
+        xs = _bracket(_SlotEnter, self.driver, fwd, bwd, xs)
+        ys = fn(*xs)
+        return _bracket(_SlotExit, self.driver, fwd, bwd, ys)
+
+    def forward(self, h: torch.Tensor) -> torch.Tensor:
+        B, S, H = h.shape
+        nh = self.heads
+        a = F.layer_norm(h, (H,))
+        wq, wk, wv = self.slots["qkv"]
+        q, k, v = self._slot("qkv", (a,), lambda x: (self._lin(x, wq), self._lin(x, wk),
+                                                     self._lin(x, wv)))
+
+        def heads(t):
+            return t.view(B, S, nh, H // nh).transpose(1, 2)
+
+        o = F.scaled_dot_product_attention(heads(q), heads(k), heads(v), is_causal=True)
+        o = o.transpose(1, 2).reshape(B, S, H)
+        (wo,) = self.slots["attn_out"]
+        (attn,) = self._slot("attn_out", (o,), lambda x: (self._lin(x, wo),))
+        h = h + attn
+        b = F.layer_norm(h, (H,))
+        w1a, w1b = self.slots["mlp_in"]
+        u1, u2 = self._slot("mlp_in", (b,), lambda x: (self._lin(x, w1a), self._lin(x, w1b)))
+        g1, g2 = F.gelu(u1, approximate="tanh"), F.gelu(u2, approximate="tanh")
+        w2a, w2b = self.slots["mlp_out"]
+        (y,) = self._slot("mlp_out", (g1, g2),
+                          lambda x1, x2: (self._lin(x1, w2a) + self._lin(x2, w2b),))
+        return h + y
+
+
+class ReferenceShapedGPT(nn.Module):
+    """GPT with tied embedding/LM head; see module docstring."""
+
+    def __init__(self, schema: ModelSchema, dtype: torch.dtype = torch.float16,
+                 grad_sink: Callable = write_grad_into_slot, placeholders: bool = False):
+        """``placeholders``: parameters start as empty tensors; their ``.data``
+        is bound to chunk slots (or embedding buffers) by the executor."""
+        super().__init__()
+        self.schema = schema
+        self.driver = EventDriver()
+        V, S, H = schema.vocab, schema.seq_len, schema.hidden_dim
+        self.wte = nn.Parameter(torch.empty(0 if placeholders else (V, H), dtype=dtype))
+        self.wpe = nn.Parameter(torch.empty(0 if placeholders else (S, H), dtype=dtype))
+        self.blocks = nn.ModuleList([GPTBlock(schema, l, self.driver, dtype, grad_sink,
+                                              placeholders)
+                                     for l in range(schema.layers)])
+        self.embedding_events = (-1, -1)
+
+    def chunk_parameters(self) -> List[nn.Parameter]:
+        """Chunk-managed parameters in tensor-id order (== param_tensor_specs)."""
+        out: List[nn.Parameter] = []
+        for blk in self.blocks:
+            for name, _ in OP_SLOTS:
+                out.extend(blk.slots[name])
+        return out
+
+    def embedding_parameters(self) -> List[nn.Parameter]:
+        return [self.wte, self.wpe]
+
+    def attach_events(self, timeline) -> None:
+        """Map every slot / the embedding to its (FWD, BWD) timeline indices."""
+        idx = {ev.name: ev.index for ev in timeline.events}
+        for blk in self.blocks:
+            for name, _ in OP_SLOTS:
+                blk.events[name] = (idx["l%d.%s.fwd" % (blk.layer, name)],
+                                    idx["l%d.%s.bwd" % (blk.layer, name)])
+        self.embedding_events = (idx["embedding.fwd"], idx["embedding.bwd"])
+
+    def forward(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        B, S = tokens.shape
+        efwd, ebwd = self.embedding_events
+        self.driver.start(efwd)
+        h = F.embedding(tokens, self.wte) + self.wpe[:S]
+        h = _EmbeddingMark.apply(self.driver, efwd, ebwd, h)
+        for blk in self.blocks:
+            h = blk(h)
+        h = F.layer_norm(h, (self.schema.hidden_dim,))
+        logits = F.linear(h, self.wte)
+        return F.cross_entropy(logits.float().view(B * S, -1), targets.reshape(B * S))
+
+
+def init_std() -> float:
+    return 0.02
+
+
+def reference_tensor_shapes(schema: ModelSchema) -> List[Tuple[int, int]]:
+    """Shapes in tensor-id order, matching param_tensor_specs numels."""
+    H = schema.hidden_dim
+    per_layer = [(H, H)] * 4 + [(2 * H, H)] * 2 + [(H, 2 * H)] * 2
+    shapes = per_layer * schema.layers
+    specs = param_tensor_specs(schema)
+    assert [a * b for a, b in shapes] == [s.numel for s in specs]
+    return shapes

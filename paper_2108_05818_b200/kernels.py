@@ -119,6 +119,21 @@ def adam_chunks_host(items, hyper: AdamHyper, state: N.CsStepState, n_threads: i
             "cs_adam_chunks_host")
 
 
+def grad_sumsq_host(grads: Sequence[Tuple[torch.Tensor, int]], n_threads: int = 0) -> float:
+    """Sum of squares of host-resident fp16/bf16 gradients (double)."""
+    if not grads:
+        return 0.0
+    arr = (N.CsGradItem * len(grads))()
+    for i, (g, n) in enumerate(grads):
+        if g.is_cuda:
+            raise ValueError("grad_sumsq_host needs host tensors")
+        arr[i] = N.CsGradItem(g.data_ptr(), n)
+    out = ctypes.c_double(0.0)
+    N.check(N.load().cs_grad_sumsq_host(arr, len(grads), _code(grads[0][0].dtype),
+                                        ctypes.byref(out), int(n_threads)), "cs_grad_sumsq_host")
+    return out.value
+
+
 def sumsq_partials() -> int:
     n = N.load().cs_sumsq_partials()
     if n <= 0:

@@ -1,0 +1,437 @@
+"""Payload executor: the physical side of the chunk-managed step on B200.
+
+The accounting core (memory / parallel / engine) decides; this class makes
+each decision real at the moment it is taken:
+
+====================================  =====================================================
+reference accounting site             realisation here
+====================================  =====================================================
+``fetch_chunk`` / ``_evict_one``      ``copy``: cudaMemcpyAsync H2D/D2H of the whole chunk
+(`memory.py:207-221, 277-301`)        payload on a dedicated copy stream between pinned
+                                      host slabs and HBM; the compute stream waits on the
+                                      copy's event only when the chunk is next *used*
+``place_payload`` / lazy OS birth     ``materialize``: an (uninitialised) payload born on
+(`memory.py:223-231`,                 the device; lazy optimizer state is initialised by
+`engine.py:234-240`)                  K6 ``cs_master_init`` reading the pinned fp32 init
+``release_chunk`` / ``note_write``    ``drop``: the payload is freed and every parameter
+                                      view into it is unbound
+``DpRuntime`` gather / reduce-scatter  NCCL ``all_gather_into_tensor`` into a p×cap group
+(`parallel.py:196-264`)               slab (remote members become views of their slot) and
+                                      ``reduce_scatter_tensor(AVG)`` of the group's grads
+``Engine._compute_event``             parameter ``.data`` re-pointed at the chunk slot
+(`engine.py:164-179`)                 before the operator runs
+``Engine._adam_event``                K2 grad sum-of-squares → device step scalars
+(`engine.py:225-272`)                 (clip / found-inf / loss scale) → ONE K1
+                                      ``cs_adam_chunks`` launch over every GPU-placed local
+                                      position (+ the embedding); host K1 for CPU-placed ones
+====================================  =====================================================
+
+Chunk payloads are flat tensors of the chunk's full capacity (the reference
+charges full capacity, `chunks.py:99-102`).  HBM comes from PyTorch's caching
+allocator (chunk-sized blocks are recycled step to step), host slabs from
+its pinned caching host allocator.
+"""
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Set, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import kernels as K
+from .chunks import Chunk, ChunkKind, ChunkSet
+from .engine import StepExecutor
+from .memory import PayloadBackend
+from .model import CPU, GPU
+from .parallel import CollectiveBackend, CommGroup, DpPartition
+
+
+class ChunkComm:
+    """Chunk-group collectives for one rank (device-agnostic plumbing over
+    ``torch.distributed``: NCCL over NVLink on the B200 box, gloo in the CPU
+    tests).  Buffers follow NCCL's layout: slot k of a p×cap group buffer is
+    rank k's chunk, which is exactly the group's position g·p+k
+    (`parallel.py:107-114`), so no reordering copy is ever needed."""
+
+    def __init__(self, group: Optional["dist.ProcessGroup"] = None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.calls: List[Tuple[str, int]] = []
+
+    def all_gather_slab(self, slab: torch.Tensor) -> None:
+        """In place: slot ``rank`` of ``slab`` is this rank's contribution."""
+        cap = slab.numel() // self.world
+        mine = slab[self.rank * cap:(self.rank + 1) * cap]
+        dist.all_gather_into_tensor(slab, mine, group=self.group)
+        self.calls.append(("all_gather", slab.numel() * slab.element_size()))
+
+    def reduce_scatter_avg(self, out: torch.Tensor, slab: torch.Tensor) -> None:
+        dist.reduce_scatter_tensor(out, slab, op=dist.ReduceOp.AVG, group=self.group)
+        self.calls.append(("reduce_scatter", slab.numel() * slab.element_size()))
+
+    def all_reduce_sum(self, t: torch.Tensor) -> None:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def all_reduce_avg(self, t: torch.Tensor) -> None:
+        dist.all_reduce(t, op=dist.ReduceOp.AVG, group=self.group)
+
+
+@dataclass
+class ExecStats:
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+    copies: int = 0
+    gathers: int = 0
+    reduce_scatters: int = 0
+    adam_launch_items: int = 0
+    host_adam_items: int = 0
+    copy_events: List[Tuple[str, int, "torch.cuda.Event", "torch.cuda.Event"]] = field(
+        default_factory=list)
+
+
+class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
+    """Owns every chunk payload of one rank and realises the engine's decisions."""
+
+    def __init__(self, device: torch.device, dtype: torch.dtype, hyper: K.AdamHyper,
+                 init_loss_scale: float = 1.0, dynamic_loss_scale: bool = False,
+                 max_grad_norm: float = 0.0, comm: Optional[ChunkComm] = None,
+                 host_threads: int = 0, time_copies: bool = False):
+        if dtype not in (torch.float16, torch.bfloat16):
+            raise TypeError("chunk dtype must be float16 or bfloat16")
+        self.device = torch.device(device)
+        self.dtype = dtype
+        self.hyper = hyper
+        self.dynamic_loss_scale = dynamic_loss_scale
+        self.max_grad_norm = max_grad_norm
+        self.comm = comm
+        self.host_threads = host_threads
+        self.time_copies = time_copies
+        self.compute = torch.cuda.current_stream(self.device)
+        self.copy_stream = torch.cuda.Stream(self.device)
+        self.state = K.StepState(self.device, init_loss_scale)
+        self.partials = torch.zeros(K.sumsq_partials() + 1, device=self.device)
+        self.payload: Dict[str, Dict[int, torch.Tensor]] = {GPU: {}, CPU: {}}
+        self.ready: Dict[Tuple[int, str], torch.cuda.Event] = {}
+        self.stats = ExecStats()
+        self._retain_req: Set[Tuple[int, str]] = set()
+        self._retained: Dict[Tuple[int, str], torch.Tensor] = {}
+        self._awaiting_gather: Set[int] = set()
+        self._group_slab: Dict[int, torch.Tensor] = {}
+        self._pending: List[Tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, int]] = []
+        self._pending_ids: Set[int] = set()
+        self._host_state = None
+        self._placeholder = torch.empty(0, dtype=dtype, device=self.device)
+        self.chunk_set: Optional[ChunkSet] = None
+        #: test hook: called as observer("pre"|"post", items) around each K1 launch
+        self.adam_observer = None
+        #: CUDA events bracketing every K1 launch (bench: in-region kernel timing)
+        self.k1_events: List[Tuple["torch.cuda.Event", "torch.cuda.Event", int]] = []
+        self.record_k1 = False
+
+    # -- wiring -------------------------------------------------------------------
+
+    def attach(self, chunk_set: ChunkSet, partition: DpPartition, rank: int,
+               params: Sequence[torch.nn.Parameter], shapes: Sequence[Tuple[int, ...]],
+               embedding: Sequence[Tuple[torch.nn.Parameter, torch.Tensor, torch.Tensor,
+                                         torch.Tensor]] = ()) -> None:
+        """Bind the layout, this rank's partition and the model's parameters
+        (``params[tid]`` has shape ``shapes[tid]``); ``embedding`` lists the
+        non-chunked (param, master, m, v) quadruples updated in the same K1."""
+        self.chunk_set, self.partition, self.rank = chunk_set, partition, rank
+        self.params, self.shapes = list(params), list(shapes)
+        self.offsets = chunk_set.element_offsets()
+        self.embedding = list(embedding)
+        self._bound: Dict[int, int] = {}  # tid -> chunk id its .data views
+        self.init32: Dict[int, torch.Tensor] = {}
+
+    def _is_remote_param(self, chunk: Chunk) -> bool:
+        return (chunk.list_kind is ChunkKind.PARAM_FP16
+                and self.partition.owner_of_position(chunk.position) != self.rank)
+
+    def _elem_dtype(self, chunk: Chunk) -> torch.dtype:
+        return self.dtype if chunk.list_kind is ChunkKind.PARAM_FP16 else torch.float32
+
+    def _alloc(self, chunk: Chunk, device: str) -> torch.Tensor:
+        if device == GPU:
+            return torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk),
+                               device=self.device)
+        return torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk), pin_memory=True)
+
+    def tensor(self, chunk: Chunk, device: str) -> torch.Tensor:
+        return self.payload[device][chunk.chunk_id]
+
+    def has(self, chunk: Chunk, device: str) -> bool:
+        return chunk.chunk_id in self.payload[device]
+
+    def seed_host_payload(self, chunk: Chunk, data: torch.Tensor) -> None:
+        """Initial CPU payload of a chunk registered with a CPU copy."""
+        assert not data.is_cuda and data.is_pinned()
+        self.payload[CPU][chunk.chunk_id] = data
+
+    # -- stream ordering ------------------------------------------------------------
+
+    def wait_ready(self, chunk: Chunk, device: str) -> None:
+        ev = self.ready.pop((chunk.chunk_id, device), None)
+        if ev is None:
+            return
+        if device == GPU:
+            self.compute.wait_event(ev)
+        else:
+            ev.synchronize()
+
+    # -- PayloadBackend ------------------------------------------------------------------
+
+    def copy(self, chunk: Chunk, src: str, dst: str, moment: int, reason: str) -> None:
+        if chunk.chunk_id in self._pending_ids:
+            self._flush_adam()
+        if src == GPU and chunk.chunk_id in self._awaiting_gather:
+            raise RuntimeError("chunk %d moved before its gather landed" % chunk.chunk_id)
+        s = self.payload[src][chunk.chunk_id]
+        d = self._retained.pop((chunk.chunk_id, dst), None)
+        if d is None:
+            d = self._alloc(chunk, dst)
+        cs = self.copy_stream
+        cs.wait_stream(self.compute)   # source final, destination block free
+        prior = self.ready.pop((chunk.chunk_id, src), None)
+        if prior is not None:
+            cs.wait_event(prior)
+        with torch.cuda.stream(cs):
+            t0 = torch.cuda.Event(enable_timing=True) if self.time_copies else None
+            if t0 is not None:
+                t0.record(cs)
+            d.copy_(s, non_blocking=True)
+            done = torch.cuda.Event(enable_timing=self.time_copies)
+            done.record(cs)
+        if src == GPU:
+            s.record_stream(cs)
+            self.stats.d2h_bytes += s.numel() * s.element_size()
+        if dst == GPU:
+            d.record_stream(cs)
+            self.stats.h2d_bytes += d.numel() * d.element_size()
+        if t0 is not None:
+            self.stats.copy_events.append(("%s>%s" % (src, dst), d.numel() * d.element_size(),
+                                           t0, done))
+        self.stats.copies += 1
+        self.ready[(chunk.chunk_id, dst)] = done
+        self.payload[dst][chunk.chunk_id] = d
+
+    def materialize(self, chunk: Chunk, device: str) -> None:
+        key = (chunk.chunk_id, device)
+        t = self._retained.pop(key, None)
+        if t is None and device == GPU and self._is_remote_param(chunk):
+            self._awaiting_gather.add(chunk.chunk_id)  # the group slab will back it
+            return
+        self.payload[device][chunk.chunk_id] = t if t is not None else self._alloc(chunk, device)
+
+    def drop(self, chunk: Chunk, device: str) -> None:
+        cid = chunk.chunk_id
+        key = (cid, device)
+        t = self.payload[device].pop(cid, None)
+        self._awaiting_gather.discard(cid)
+        ev = self.ready.pop(key, None)
+        if key in self._retain_req:
+            self._retain_req.discard(key)
+            if t is not None:
+                if ev is not None:
+                    self.ready[key] = ev
+                self._retained[key] = t
+        if device == GPU and chunk.list_kind is ChunkKind.PARAM_FP16:
+            for tmeta in chunk.tensors:
+                if self._bound.get(tmeta.tensor_id) == cid:
+                    self.params[tmeta.tensor_id].data = self._placeholder
+                    del self._bound[tmeta.tensor_id]
+            if self._is_remote_param(chunk):
+                self._maybe_free_slab(chunk)
+
+    def _maybe_free_slab(self, chunk: Chunk) -> None:
+        gid = chunk.position // self.partition.nproc
+        if gid not in self._group_slab:
+            return
+        group = self.partition.groups[gid]
+        alive = any(self.chunk_set.param_chunk(p).chunk_id in self.payload[GPU]
+                    for p in group.real_positions
+                    if self.partition.owner_of_position(p) != self.rank)
+        if not alive:
+            del self._group_slab[gid]
+
+    # -- CollectiveBackend -----------------------------------------------------------------
+
+    def _group_slot(self, slab: torch.Tensor, k: int) -> torch.Tensor:
+        cap = self.chunk_set.capacity_elems
+        return slab[k * cap:(k + 1) * cap]
+
+    def all_gather(self, group: CommGroup, kind: str) -> None:
+        if self.comm is None:
+            raise RuntimeError("data-parallel gather without a communicator")
+        cap, p = self.chunk_set.capacity_elems, self.partition.nproc
+        slab = torch.empty(p * cap, dtype=self.dtype, device=self.device)
+        mine = self._group_slot(slab, self.rank)
+        pos = group.member_positions[self.rank]
+        if pos is None:
+            mine.zero_()  # phantom slot of a padded tail group
+        else:
+            local = self.chunk_set.param_chunk(pos)
+            if self.has(local, GPU):
+                self.wait_ready(local, GPU)
+                mine.copy_(self.tensor(local, GPU))
+            else:  # local payload lives on the host: stage it into our slot
+                self.wait_ready(local, CPU)
+                mine.copy_(self.tensor(local, CPU), non_blocking=True)
+        self.comm.all_gather_slab(slab)
+        for k, q in enumerate(group.member_positions):
+            if q is None or k == self.rank:
+                continue
+            remote = self.chunk_set.param_chunk(q)
+            self.payload[GPU][remote.chunk_id] = self._group_slot(slab, k)
+            self.ready.pop((remote.chunk_id, GPU), None)
+            self._awaiting_gather.discard(remote.chunk_id)
+        self._group_slab[group.group_id] = slab
+        self.stats.gathers += 1
+
+    def reduce_scatter(self, group: CommGroup) -> None:
+        if self.comm is None:
+            raise RuntimeError("data-parallel reduce-scatter without a communicator")
+        cap, p = self.chunk_set.capacity_elems, self.partition.nproc
+        slab = self._group_slab.get(group.group_id)
+        if slab is None:
+            slab = torch.empty(p * cap, dtype=self.dtype, device=self.device)
+        out = None
+        for k, q in enumerate(group.member_positions):
+            slot = self._group_slot(slab, k)
+            if q is None:
+                if k == self.rank:
+                    slot.zero_()
+                continue
+            member = self.chunk_set.param_chunk(q)
+            src = self.tensor(member, GPU)
+            if k == self.rank:
+                out = src
+            if src.data_ptr() != slot.data_ptr():
+                self.wait_ready(member, GPU)
+                slot.copy_(src)
+        if out is None:
+            out = torch.empty(cap, dtype=self.dtype, device=self.device)  # phantom owner
+        self.comm.reduce_scatter_avg(out, slab)
+        self._group_slab[group.group_id] = slab
+        self.stats.reduce_scatters += 1
+
+    # -- StepExecutor ---------------------------------------------------------------------------
+
+    def on_compute_start(self, ev, chunks: Sequence[Chunk]) -> None:
+        for chunk in chunks:
+            if chunk.chunk_id in self._awaiting_gather:
+                raise RuntimeError("chunk %d computes before its gather" % chunk.chunk_id)
+            self.wait_ready(chunk, GPU)
+        cs, gpu = self.chunk_set, self.payload[GPU]
+        for tid in ev.tensor_refs:
+            pos, off, n = self.offsets[tid]
+            cid = cs.param_chunk(pos).chunk_id
+            self.params[tid].data = gpu[cid][off:off + n].view(self.shapes[tid])
+            self._bound[tid] = cid
+
+    def on_adam_begin(self, iteration: int) -> None:
+        """Global grad norm / found-inf and the device step scalars."""
+        cs = self.chunk_set
+        self._host_state = None
+        emb_grads = []
+        for param, _, _, _ in self.embedding:
+            if param.grad is None:
+                raise RuntimeError("embedding parameter has no gradient at ADAM")
+            if self.comm is not None and self.comm.world > 1:
+                self.comm.all_reduce_avg(param.grad)
+            emb_grads.append((param.grad, param.grad.numel()))
+        dev_items, host_items = [], []
+        for pos in self.partition.local_positions(self.rank):
+            chunk = cs.param_chunk(pos)
+            n = chunk.used_elems
+            if self.has(chunk, GPU):
+                self.wait_ready(chunk, GPU)
+                dev_items.append((self.tensor(chunk, GPU), n))
+            else:
+                self.wait_ready(chunk, CPU)
+                host_items.append((self.tensor(chunk, CPU), n))
+        if self.comm is None or self.comm.rank == 0:
+            dev_items += emb_grads  # replicated after the all-reduce: count once
+        host = K.grad_sumsq_host(host_items, self.host_threads) if host_items else 0.0
+        self.partials[-1:].fill_(host)
+        K.grad_sumsq(dev_items, self.partials[:-1], dtype=self.dtype)
+        K.sumsq_finalize(self.partials, self.state)
+        if self.comm is not None and self.comm.world > 1:
+            self.comm.all_reduce_sum(self.state.sumsq())
+        K.adam_prepare(self.state, self.hyper, max_grad_norm=self.max_grad_norm,
+                       dynamic_scale=self.dynamic_loss_scale)
+        # non-chunked embedding: its autograd gradient is packed over the
+        # parameter (K3) so it follows the same in-place update as a chunk
+        for param, master, m, v in self.embedding:
+            flat = param.data.view(-1)
+            K.pack([(flat, 0, param.grad.view(-1), flat.numel())])
+            param.grad = None
+            self._pending.append((flat, master, m, v, flat.numel()))
+
+    def init_optimizer_state(self, position: int, device: str) -> None:
+        p32, m, v = (self.tensor(c, device) for c in self.chunk_set.os_triplet(position))
+        src = self.init32.pop(position)
+        n = self.chunk_set.param_chunk(position).used_elems
+        if device == GPU:
+            K.master_init(p32, m, v, src, n)   # K6 reads the pinned fp32 init in place
+            self._keepalive = getattr(self, "_keepalive", [])
+            self._keepalive.append(src)
+        else:
+            p32[:n].copy_(src[:n])
+            m.zero_()
+            v.zero_()
+
+    def adam_position(self, position: int, device: str) -> None:
+        cs = self.chunk_set
+        param = cs.param_chunk(position)
+        triplet = cs.os_triplet(position)
+        n = param.used_elems
+        if device == GPU:
+            for c in (param,) + triplet:
+                self.wait_ready(c, GPU)
+            p16 = self.tensor(param, GPU)
+            p32, m, v = (self.tensor(c, GPU) for c in triplet)
+            self._pending.append((p16, p32, m, v, n))
+            self._pending_ids.update(c.chunk_id for c in (param,) + triplet)
+            return
+        if self._host_state is None:
+            self._host_state = self.state.read()  # one sync per step, only with host positions
+        for c in (param,) + triplet:
+            self.wait_ready(c, CPU)
+        p16 = self.tensor(param, CPU)
+        p32, m, v = (self.tensor(c, CPU) for c in triplet)
+        K.adam_chunks_host([(p16, p32, m, v, n)], self.hyper, self._host_state,
+                           self.host_threads)
+        self.stats.host_adam_items += 1
+
+    def retain_param_payload(self, chunk: Chunk, device: str) -> None:
+        self._retain_req.add((chunk.chunk_id, device))
+
+    def _flush_adam(self) -> None:
+        if self._pending:
+            if self.adam_observer is not None:
+                self.adam_observer("pre", self._pending)
+            if self.record_k1:
+                t0 = torch.cuda.Event(enable_timing=True)
+                t1 = torch.cuda.Event(enable_timing=True)
+                t0.record(self.compute)
+            K.adam_chunks(self._pending, self.hyper, self.state)
+            if self.record_k1:
+                t1.record(self.compute)
+                self.k1_events.append((t0, t1, sum(it[4] for it in self._pending)))
+            if self.adam_observer is not None:
+                self.adam_observer("post", self._pending)
+            self.stats.adam_launch_items += len(self._pending)
+        self._pending = []
+        self._pending_ids = set()
+
+    def on_adam_end(self) -> None:
+        self._flush_adam()
+        self._retain_req.clear()
+        self._retained.clear()
+
+    def end_of_warmup(self) -> None:
+        """The fp32 init copies read zero-copy by K6 can go once it has run."""
+        torch.cuda.synchronize(self.device)
+        self._keepalive = []

@@ -1,0 +1,203 @@
+"""ChunkTrainer: the chunk-managed GPT training step on B200 (the public API).
+
+Wiring (one process per GPU):
+
+* the accounting is the reference's own ``Simulator`` wiring
+  (`/root/reference/pkg/src/chunkstar/scenario.py:105-182`) — layout, DP
+  partition, fp16 params initialised on the host, lazily born optimizer
+  state, GPU and CPU pools, manager, DP runtime, engine — with the payload
+  executor attached as payload / collective / step backend;
+* the model is the reference-shaped GPT (:mod:`.gpt`); its slot markers call
+  :meth:`Engine.start_event` / :meth:`Engine.finish_event`, so forward and
+  backward run the timeline's events in order and every fetch, eviction,
+  gather, reduce-scatter and parameter re-binding happens at the reference's
+  decision point;
+* the ADAM event runs the device-side K2 → step scalars → one K1 launch.
+
+Warm-up (iteration 0) uses list-order eviction, the 0.8 soft limit and
+records the access trace; the placement plan is computed at its ADAM event
+(`engine.py:282-333`); later iterations use the configured strategy.
+"""
+
+import os
+from typing import Callable, List, Optional, Tuple
+
+import torch
+
+from . import kernels as K
+from .chunks import ChunkKind
+from .config import HardwareSpec, PolicySpec
+from .engine import IterationReport
+from .gpt import ReferenceShapedGPT, reference_tensor_shapes
+from .memory import OOMError
+from .model import ModelSchema
+from .payload import ChunkComm, ChunkPayloadExecutor
+from .scenario import Simulator
+
+
+def _host_ram_bytes() -> int:
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        return 256 * 10**9
+
+
+class ChunkTrainer:
+    """Chunk-managed (PatrickStar) data-parallel GPT training on one GPU per rank."""
+
+    def __init__(self, schema: ModelSchema, policy: Optional[PolicySpec] = None,
+                 hardware: Optional[HardwareSpec] = None, dtype: torch.dtype = torch.float16,
+                 seed: int = 0, hyper: Optional[K.AdamHyper] = None,
+                 device: Optional[torch.device] = None,
+                 process_group=None, max_grad_norm: float = 0.0,
+                 init_loss_scale: Optional[float] = None,
+                 dynamic_loss_scale: Optional[bool] = None,
+                 non_model_fn: Optional[Callable[[int], int]] = None,
+                 host_threads: int = 0, time_copies: bool = False):
+        if not torch.cuda.is_available():
+            raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
+        self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
+        torch.cuda.set_device(self.device)
+        self.schema = schema
+        self.dtype = dtype
+        self.policy = policy or PolicySpec()
+        comm = None
+        nproc, rank = 1, 0
+        if process_group is not None or (torch.distributed.is_initialized()
+                                         and torch.distributed.get_world_size() > 1):
+            comm = ChunkComm(process_group)
+            nproc, rank = comm.world, comm.rank
+        if hardware is None:
+            total = torch.cuda.get_device_properties(self.device).total_memory
+            hardware = HardwareSpec(gpu_count=nproc, gpu_bytes=int(total * 0.9),
+                                    cpu_bytes=int(_host_ram_bytes() * 0.8))
+        fp16 = dtype == torch.float16
+        if dynamic_loss_scale is None:
+            dynamic_loss_scale = fp16
+        if init_loss_scale is None:
+            init_loss_scale = 2.0 ** 16 if dynamic_loss_scale else 1.0
+        self.hyper = hyper or K.AdamHyper(lr=1e-4, betas=(0.9, 0.999), eps=1e-8)
+        self.executor = ChunkPayloadExecutor(
+            self.device, dtype, self.hyper, init_loss_scale=init_loss_scale,
+            dynamic_loss_scale=dynamic_loss_scale, max_grad_norm=max_grad_norm, comm=comm,
+            host_threads=host_threads, time_copies=time_copies)
+        ex = self.executor
+        self.sim = Simulator(schema, hardware, self.policy, nproc=nproc, rank=rank,
+                             payload_backend=ex, collective_backend=ex, executor=ex,
+                             non_model_fn=non_model_fn)
+        self.nproc, self.rank = nproc, rank
+        with torch.device(self.device):
+            self.model = ReferenceShapedGPT(schema, dtype=dtype, placeholders=True)
+        self.shapes = reference_tensor_shapes(schema)
+        self.model.attach_events(self.sim.timeline)
+        self._events = self.sim.timeline.events
+        self.model.driver.on_start = self._on_start
+        self.model.driver.on_finish = self._on_finish
+        emb = []
+        emb_shapes = [(schema.vocab, schema.hidden_dim), (schema.seq_len, schema.hidden_dim)]
+        for p, shape in zip(self.model.embedding_parameters(), emb_shapes):
+            master = torch.empty(shape, dtype=torch.float32, device=self.device)
+            emb.append((p, master, torch.zeros_like(master), torch.zeros_like(master)))
+        ex.attach(self.sim.chunk_set, self.sim.partition, rank,
+                  self.model.chunk_parameters(), self.shapes,
+                  [(p, mst.view(-1), m.view(-1), v.view(-1)) for p, mst, m, v in emb])
+        self._init_weights(seed, emb)
+        self.iteration = 0
+        self.reports: List[IterationReport] = []
+
+    # -- initialisation ---------------------------------------------------------------
+
+    def _init_weights(self, seed: int, emb) -> None:
+        """N(0, 0.02) weights, a pure function of (seed, tensor id): identical
+        for every world size.  Each local fp16 chunk is cast+packed (K5) on
+        the GPU, then lands in its pinned host slab (`scenario.py:126`
+        initialises fp16 params on the CPU); the fp32 values are kept in a
+        pinned buffer from which K6 births the master copy at the first ADAM."""
+        cs, ex = self.sim.chunk_set, self.executor
+        cap = cs.capacity_elems
+        staging32 = torch.empty(cap, dtype=torch.float32, device=self.device)
+        staging16 = torch.empty(cap, dtype=self.dtype, device=self.device)
+        gen = torch.Generator(device=self.device)
+        for pos in self.sim.local:
+            chunk = cs.param_chunk(pos)
+            items = []
+            for t in chunk.tensors:
+                gen.manual_seed(seed * 1_000_003 + t.tensor_id)
+                sl = staging32[t.offset_elems:t.offset_elems + t.numel]
+                sl.normal_(0.0, 0.02, generator=gen)
+                items.append((staging16, t.offset_elems, sl, t.numel))
+            K.cast_pack(items)
+            host16 = torch.empty(cap, dtype=self.dtype, pin_memory=True)
+            host32 = torch.empty(cap, dtype=torch.float32, pin_memory=True)
+            host16.copy_(staging16)
+            host32.copy_(staging32)
+            ex.seed_host_payload(chunk, host16)
+            ex.init32[pos] = host32
+        n_chunked = len(self.shapes)
+        for k, (p, master, m, v) in enumerate(emb):
+            gen.manual_seed(seed * 1_000_003 + n_chunked + k)
+            master.normal_(0.0, 0.02, generator=gen)
+            p.data = torch.empty(master.shape, dtype=self.dtype, device=self.device)
+            K.cast_pack([(p.data.view(-1), 0, master.view(-1), master.numel())])
+        torch.cuda.synchronize(self.device)
+
+    # -- event plumbing ---------------------------------------------------------------------
+
+    def _check(self) -> None:
+        if self.sim.engine.iteration_failed:
+            r = self.sim.engine._it.report
+            raise OOMError("gpu" if r.failure_reason == "GPU_OOM" else "cpu",
+                           r.failure_moment or -1, 0, 0)
+
+    def _on_start(self, idx: int) -> None:
+        self.sim.engine.start_event(self._events[idx])
+        self._check()
+
+    def _on_finish(self, idx: int) -> None:
+        self.sim.engine.finish_event(self._events[idx])
+        self._check()
+
+    # -- the step -----------------------------------------------------------------------------
+
+    def step(self, tokens: torch.Tensor) -> torch.Tensor:
+        """One training iteration on device-resident tokens [B, S+1] (int64).
+
+        Returns the (unscaled) loss as a device scalar; no host sync."""
+        eng = self.sim.engine
+        warm = self.iteration == 0
+        eng.begin_iteration(self.iteration, warm,
+                            self.sim._plan_builder() if warm else None, self.sim.local)
+        self._check()
+        inp, tgt = tokens[:, :-1], tokens[:, 1:]
+        loss = self.model(inp, tgt)
+        (loss * self.executor.state.loss_scale()).backward()
+        adam = self._events[-1]
+        eng.start_event(adam)
+        self._check()
+        eng.finish_event(adam)
+        self._check()
+        report = eng.end_iteration()
+        self.reports.append(report)
+        if warm:
+            self.executor.end_of_warmup()
+        self.iteration += 1
+        return loss.detach()
+
+    def step_host(self, tokens_host: torch.Tensor) -> float:
+        """End-to-end step from host memory: H2D tokens, step, D2H loss."""
+        tokens = tokens_host.to(self.device, non_blocking=True)
+        return float(self.step(tokens).item())
+
+    # -- inspection -----------------------------------------------------------------------------
+
+    def step_state(self):
+        return self.executor.state.read()
+
+    def local_chunk_payload(self, position: int, kind: ChunkKind = ChunkKind.PARAM_FP16):
+        """The current payload (device preferred) of a local chunk position."""
+        chunk = self.sim.chunk_set.chunk_at(kind, position)
+        ex = self.executor
+        for dev in ("gpu", "cpu"):
+            if ex.has(chunk, dev):
+                return ex.tensor(chunk, dev)
+        return None
