@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-batch", type=int, default=1)
+    ap.add_argument("--profile-step", action="store_true",
+                    help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
+                         "(for ncu --profile-from-start off); prints no bench line")
     return ap.parse_args()
 
 
@@ -212,6 +215,12 @@ def main():
         trainer.step(dev_pool[i % 4])
     torch.cuda.synchronize()
     barrier()
+    if args.profile_step:
+        torch.cuda.cudart().cudaProfilerStart()
+        trainer.step(dev_pool[0])
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        return
 
     # ---- timed region 1: device-resident inputs -> value -----------------------
     ex.record_k1 = True
