@@ -107,10 +107,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.comm = comm
         self.host_threads = host_threads
         self.time_copies = time_copies
-        self.compute = torch.cuda.current_stream(self.device)
-        self.copy_stream = torch.cuda.Stream(self.device)
-        self.state = K.StepState(self.device, init_loss_scale)
-        self.partials = torch.zeros(K.sumsq_partials() + 1, device=self.device)
+        self._setup_device(init_loss_scale)
         self.payload: Dict[str, Dict[int, torch.Tensor]] = {GPU: {}, CPU: {}}
         self.ready: Dict[Tuple[int, str], torch.cuda.Event] = {}
         self.stats = ExecStats()
@@ -128,6 +125,12 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         #: CUDA events bracketing every K1 launch (bench: in-region kernel timing)
         self.k1_events: List[Tuple["torch.cuda.Event", "torch.cuda.Event", int]] = []
         self.record_k1 = False
+
+    def _setup_device(self, init_loss_scale: float) -> None:
+        self.compute = torch.cuda.current_stream(self.device)
+        self.copy_stream = torch.cuda.Stream(self.device)
+        self.state = K.StepState(self.device, init_loss_scale)
+        self.partials = torch.zeros(K.sumsq_partials() + 1, device=self.device)
 
     # -- wiring -------------------------------------------------------------------
 
@@ -184,16 +187,25 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def copy(self, chunk: Chunk, src: str, dst: str, moment: int, reason: str) -> None:
         if chunk.chunk_id in self._pending_ids:
-            self._flush_adam()
+            self._flush_adam()  # the move must carry post-update bytes
         if src == GPU and chunk.chunk_id in self._awaiting_gather:
             raise RuntimeError("chunk %d moved before its gather landed" % chunk.chunk_id)
         s = self.payload[src][chunk.chunk_id]
         d = self._retained.pop((chunk.chunk_id, dst), None)
         if d is None:
             d = self._alloc(chunk, dst)
+        prior = self.ready.pop((chunk.chunk_id, src), None)
+        done = self._transfer(s, d, src, dst, prior)
+        if done is not None:
+            self.ready[(chunk.chunk_id, dst)] = done
+        self.payload[dst][chunk.chunk_id] = d
+
+    def _transfer(self, s: torch.Tensor, d: torch.Tensor, src: str, dst: str,
+                  prior: Optional["torch.cuda.Event"]):
+        """cudaMemcpyAsync of a whole payload on the copy stream; returns the
+        completion event consumers wait on (`wait_ready`)."""
         cs = self.copy_stream
         cs.wait_stream(self.compute)   # source final, destination block free
-        prior = self.ready.pop((chunk.chunk_id, src), None)
         if prior is not None:
             cs.wait_event(prior)
         with torch.cuda.stream(cs):
@@ -213,8 +225,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.stats.copy_events.append(("%s>%s" % (src, dst), d.numel() * d.element_size(),
                                            t0, done))
         self.stats.copies += 1
-        self.ready[(chunk.chunk_id, dst)] = done
-        self.payload[dst][chunk.chunk_id] = d
+        return done
 
     def materialize(self, chunk: Chunk, device: str) -> None:
         key = (chunk.chunk_id, device)
