@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--vocab", type=int, default=50304)
     ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--no-graph", action="store_true",
+                    help="eager steps only (no CUDA-graph replay of the steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-batch", type=int, default=1)
     ap.add_argument("--profile-step", action="store_true",
@@ -199,7 +201,8 @@ def main():
     schema = build_gpt_schema(**schema_kw)
     dtype = torch.float16 if args.dtype == "fp16" else torch.bfloat16
     trainer = ChunkTrainer(schema, PolicySpec(capacity_elems=args.cap), dtype=dtype, seed=0,
-                           hyper=K.AdamHyper(lr=1e-4, betas=(0.9, 0.999), eps=1e-8))
+                           hyper=K.AdamHyper(lr=1e-4, betas=(0.9, 0.999), eps=1e-8),
+                           cuda_graph=not args.no_graph)
     ex = trainer.executor
     B, S = args.batch, args.seq
     gen = torch.Generator().manual_seed(1000 + rank)
@@ -213,6 +216,9 @@ def main():
 
     for i in range(max(args.warmup, 1)):
         trainer.step(dev_pool[i % 4])
+    if trainer.cuda_graph:  # reach the fixed point and capture before timing
+        while trainer._graph is None and trainer.iteration < args.warmup + 6:
+            trainer.step(dev_pool[trainer.iteration % 4])
     torch.cuda.synchronize()
     barrier()
     if args.profile_step:
@@ -232,18 +238,25 @@ def main():
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    h0 = time.perf_counter()
     t0.record()
     for k in range(args.steps):
         loss = trainer.step(dev_pool[k % 4])
     t1.record()
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     launches = _native.launch_count() - launches0
+    if trainer._graph is not None:  # library kernels replayed from the captured graph
+        launches += trainer.graph_kernels_per_step * args.steps
     ms = t0.elapsed_time(t1) / args.steps
     ex.record_k1 = False
     k1_ms = [a.elapsed_time(b) for a, b, _ in ex.k1_events]
     k1_elems = [n for _, _, n in ex.k1_events]
+    if trainer._graph is not None and trainer.graph_k1 is not None:
+        a, b, n = trainer.graph_k1  # the K1 node of the last replay in the timed region
+        k1_ms, k1_elems = [a.elapsed_time(b)], [n]
     final_loss = float(loss.item())
     if world > 1:
         tt = torch.tensor([ms], device=dev)
@@ -300,6 +313,8 @@ def main():
                 "h2d_bytes_per_step": pool[0].numel() * pool[0].element_size(),
                 "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_ms, 3)},
         "gpu_launches": int(launches),
+        "host_enqueue_ms_per_step": round(host_ms, 3),
+        "cuda_graph": trainer._graph is not None,
         "clocks": clk,
         "final_loss": final_loss, "loss_scale": st.loss_scale, "adam_steps": int(st.step),
     }

@@ -24,14 +24,21 @@
 #include <cuda_runtime.h>
 
 #include <math.h>
+#include <stdlib.h>
 
 #include "cs_internal.h"
 
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kGroups = 4;   // 4-element groups per thread per block tile
+constexpr int kGroups = 4;   // 4-element groups per thread per block tile (K2)
 constexpr int kBlockTile = kThreads * kGroups * 4;
+// K1 tiling variants (groups per thread, min resident CTAs per SM -> register
+// cap).  Selected once per process (CS_ADAM_VARIANT, default kAdamDefault);
+// every variant computes bit-identical results.
+struct AdamVariant { int groups, min_blocks; };
+constexpr AdamVariant kAdamVariants[] = {{4, 1}, {4, 4}, {2, 4}, {2, 6}, {8, 2}};
+constexpr int kAdamDefault = 0;
 
 struct AdamBatch {
   CsAdamItem item[cs::kMaxBatch];
@@ -121,9 +128,10 @@ __device__ __forceinline__ int find_item(const int64_t* start, int n, int64_t ti
   return lo;
 }
 
-template <int DT>
-__global__ void __launch_bounds__(kThreads)
+template <int DT, int G, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
 adam_chunks_kernel(const __grid_constant__ AdamBatch b, const CsStepState* __restrict__ st) {
+  constexpr int kTile = kThreads * G * 4;
   if (st->skip) return;  // non-finite gradients: the whole step is skipped
   AdamConsts c;
   c.grad_scale = st->grad_scale;
@@ -141,14 +149,14 @@ adam_chunks_kernel(const __grid_constant__ AdamBatch b, const CsStepState* __res
   for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
     const int k = find_item(b.tile_start, b.n, tile);
     const CsAdamItem it = b.item[k];
-    const int64_t base = (tile - b.tile_start[k]) * kBlockTile;
+    const int64_t base = (tile - b.tile_start[k]) * kTile;
     uint16_t* __restrict__ p16 = static_cast<uint16_t*>(it.p16);
 
-    if (base + kBlockTile <= it.n) {  // full tile: vector path
-      uint2 g[kGroups];
-      float4 p[kGroups], m[kGroups], v[kGroups];
+    if (base + kTile <= it.n) {  // full tile: vector path
+      uint2 g[G];
+      float4 p[G], m[G], v[G];
 #pragma unroll
-      for (int u = 0; u < kGroups; ++u) {
+      for (int u = 0; u < G; ++u) {
         const int64_t e = base + (int64_t)(u * kThreads + threadIdx.x) * 4;
         g[u] = __ldcs(reinterpret_cast<const uint2*>(p16 + e));
         p[u] = __ldcs(reinterpret_cast<const float4*>(it.p32 + e));
@@ -156,7 +164,7 @@ adam_chunks_kernel(const __grid_constant__ AdamBatch b, const CsStepState* __res
         v[u] = __ldcs(reinterpret_cast<const float4*>(it.v + e));
       }
 #pragma unroll
-      for (int u = 0; u < kGroups; ++u) {
+      for (int u = 0; u < G; ++u) {
         const float4 gf = widen4<DT>(g[u]);
         adam1(gf.x, p[u].x, m[u].x, v[u].x, c);
         adam1(gf.y, p[u].y, m[u].y, v[u].y, c);
@@ -169,7 +177,7 @@ adam_chunks_kernel(const __grid_constant__ AdamBatch b, const CsStepState* __res
         __stcs(reinterpret_cast<uint2*>(p16 + e), narrow4<DT>(p[u]));
       }
     } else {  // the last, partial tile of an item
-      for (int u = 0; u < kGroups; ++u) {
+      for (int u = 0; u < G; ++u) {
         const int64_t e0 = base + (int64_t)(u * kThreads + threadIdx.x) * 4;
         for (int64_t e = e0; e < e0 + 4 && e < it.n; ++e) {
           float pp = it.p32[e], mm = it.m[e], vv = it.v[e];
@@ -305,7 +313,31 @@ __global__ void adam_prepare_kernel(CsStepState* st, CsAdamHyper h, float max_no
 // ---- host side ---------------------------------------------------------------
 
 int g_num_sms = 0;
+int g_adam_variant = -1;
 int g_adam_blocks_per_sm = 0;
+
+typedef void (*AdamKernel)(const AdamBatch, const CsStepState*);
+
+template <int DT>
+AdamKernel adam_kernel_for(int v) {
+  switch (v) {
+    case 1: return adam_chunks_kernel<DT, 4, 4>;
+    case 2: return adam_chunks_kernel<DT, 2, 4>;
+    case 3: return adam_chunks_kernel<DT, 2, 6>;
+    case 4: return adam_chunks_kernel<DT, 8, 2>;
+    default: return adam_chunks_kernel<DT, 4, 1>;
+  }
+}
+
+int adam_variant() {
+  if (g_adam_variant < 0) {
+    const char* e = getenv("CS_ADAM_VARIANT");
+    const int v = e ? atoi(e) : kAdamDefault;
+    g_adam_variant = (v >= 0 && v < (int)(sizeof(kAdamVariants) / sizeof(kAdamVariants[0])))
+                         ? v : kAdamDefault;
+  }
+  return g_adam_variant;
+}
 
 int num_sms() {
   if (g_num_sms > 0) return g_num_sms;
@@ -349,9 +381,13 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
     cs::set_error("cs_adam_chunks: no CUDA device");
     return CS_EINVAL;
   }
+  const int variant = adam_variant();
+  const int64_t tile_elems = (int64_t)kThreads * kAdamVariants[variant].groups * 4;
+  AdamKernel kern = dtype == CS_FP16 ? adam_kernel_for<CS_FP16>(variant)
+                                     : adam_kernel_for<CS_BF16>(variant);
   if (g_adam_blocks_per_sm == 0) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, adam_chunks_kernel<CS_FP16>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, 0);
     g_adam_blocks_per_sm = nb > 0 ? nb : 1;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -373,7 +409,7 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
       if (it.n == 0) continue;
       b.item[b.n] = it;
       b.tile_start[b.n] = tiles;
-      tiles += (it.n + kBlockTile - 1) / kBlockTile;
+      tiles += (it.n + tile_elems - 1) / tile_elems;
       ++b.n;
     }
     b.tile_start[b.n] = tiles;
@@ -387,10 +423,7 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
     b.adamw = hyper->adamw;
     const int64_t grid64 = (int64_t)sms * g_adam_blocks_per_sm;
     const int grid = (int)(tiles < grid64 ? tiles : grid64);
-    if (dtype == CS_FP16)
-      adam_chunks_kernel<CS_FP16><<<grid, kThreads, 0, s>>>(b, d_state);
-    else
-      adam_chunks_kernel<CS_BF16><<<grid, kThreads, 0, s>>>(b, d_state);
+    kern<<<grid, kThreads, 0, s>>>(b, d_state);
     cs::note_launches(1);
     if (int e = launch_error("cs_adam_chunks")) return e;
   }

@@ -423,13 +423,14 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         if self._pending:
             if self.adam_observer is not None:
                 self.adam_observer("pre", self._pending)
-            if self.record_k1:
-                t0 = torch.cuda.Event(enable_timing=True)
-                t1 = torch.cuda.Event(enable_timing=True)
-                t0.record(self.compute)
+            if self.record_k1:  # inside a graph capture these become event-record nodes
+                ext = torch.cuda.is_current_stream_capturing()
+                t0 = torch.cuda.Event(enable_timing=True, external=ext)
+                t1 = torch.cuda.Event(enable_timing=True, external=ext)
+                t0.record()
             K.adam_chunks(self._pending, self.hyper, self.state)
             if self.record_k1:
-                t1.record(self.compute)
+                t1.record()
                 self.k1_events.append((t0, t1, sum(it[4] for it in self._pending)))
             if self.adam_observer is not None:
                 self.adam_observer("post", self._pending)

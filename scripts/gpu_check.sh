@@ -1,7 +1,6 @@
-set -x
-python -m pytest tests -m gpu -q 2>&1 | tail -5
-ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_r1.csv python bench.py --profile-step --warmup 2 --no-cpu-baseline > gpurun_out/launches_r1.log 2>&1
-tail -2 gpurun_out/launches_r1.log
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:adam_chunks -c 1 -o gpurun_out/k1_insitu_r1 python bench.py --profile-step --warmup 2 --no-cpu-baseline > gpurun_out/ncu_k1_insitu.log 2>&1
-tail -2 gpurun_out/ncu_k1_insitu.log
-timeout 900 python bench.py --steps 10 --warmup 3 2>&1 | tail -3 | tee gpurun_out/bench_r1.json
+python -m pytest tests/test_step_gpu.py tests/test_kernels_gpu.py -q -x 2>&1 | tail -4
+for v in 0 1 2 3 4; do
+  echo "variant $v"
+  CS_ADAM_VARIANT=$v python -m paper_2108_05818_b200.microbench --sizes 30 --iters 10 2>&1 | grep adam
+  CS_ADAM_VARIANT=$v timeout 600 python bench.py --steps 6 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['ms_per_step'], d['value'], d['roofline']['achieved'], d['roofline']['frac'], d['roofline']['avg_launch_ms'], d['clocks'], d['final_loss'], d['cuda_graph'])"
+done

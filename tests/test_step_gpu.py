@@ -112,3 +112,30 @@ def test_loss_decreases_on_repeated_batch():
     batch = _tokens(schema, 1)[0]
     losses = [tr.step_host(batch) for _ in range(8)]
     assert losses[-1] < losses[0] - 0.05, losses
+
+
+def test_cuda_graph_replay_matches_eager_steps():
+    """Steady-state CUDA-graph replay is bit-identical to eager steps and the
+    accounting still produces every iteration's (unchanged) ledger."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_cap256Ki"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 8)
+    out = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for graph in (False, True):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0, cuda_graph=graph)
+            losses = [tr.step_host(t) for t in toks]
+            params = [tr.local_chunk_payload(p).cpu().clone()
+                      for p in range(tr.sim.chunk_set.positions)]
+            out[graph] = (losses, params, tr)
+    assert out[True][2]._graph is not None and out[False][2]._graph is None
+    assert out[True][0] == out[False][0]
+    for a, b in zip(out[True][1], out[False][1]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    ref = CASES["tiny_cap256Ki"]["ranks"]["0"]["iterations"][-1]
+    for r in out[True][2].reports[2:]:
+        assert _ledger(r)["transfers"] == ref["transfers"]
+        assert _ledger(r)["samples"] == ref["samples"]
