@@ -176,6 +176,17 @@ int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
 int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtype, double* out,
                        int n_threads);
 
+/* ---- fused LM-head cross entropy (the GPT step's loss) ----------------------
+ * Forward: per-row loss = logsumexp(logits_row) - logits_row[target] and the
+ * row's logsumexp, one pass over fp16/bf16 logits [rows, vocab].  Backward:
+ * logits <- (softmax - onehot) * (*dloss) * scale, in place.  dloss is a
+ * device scalar (the upstream gradient, e.g. the loss scale). */
+int cs_xent_fwd(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab,
+                int dtype, float* loss_rows, float* lse_rows, void* stream);
+int cs_xent_bwd(void* logits, const int64_t* targets, const float* lse_rows,
+                const float* dloss, float scale, int64_t rows, int64_t vocab, int dtype,
+                void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,6 +72,12 @@ SIGNATURES = {
                                            ctypes.POINTER(CsStepState), ctypes.c_int]),
     "cs_grad_sumsq_host": (ctypes.c_int, [ctypes.POINTER(CsGradItem), ctypes.c_int, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_double), ctypes.c_int]),
+    "cs_xent_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                   ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p]),
+    "cs_xent_bwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_float, ctypes.c_int64,
+                                   ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

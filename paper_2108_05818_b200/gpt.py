@@ -57,6 +57,51 @@ class _ChunkLinearFn(torch.autograd.Function):
         return dx, None, None
 
 
+class _ChunkLinearResFn(torch.autograd.Function):
+    """y = residual + x W^T with the add in the GEMM epilogue (beta = 1)."""
+
+    @staticmethod
+    def forward(ctx, x: torch.Tensor, weight: nn.Parameter, residual: torch.Tensor,
+                grad_sink: Callable):
+        ctx.weight = weight
+        ctx.grad_sink = grad_sink
+        ctx.save_for_backward(x)
+        shp = residual.shape
+        out = torch.addmm(residual.reshape(-1, shp[-1]), x.reshape(-1, x.shape[-1]), weight.t())
+        return out.view(shp)
+
+    @staticmethod
+    def backward(ctx, dy: torch.Tensor):
+        (x,) = ctx.saved_tensors
+        w = ctx.weight
+        dx = dy.matmul(w)
+        ctx.grad_sink(w, dy.reshape(-1, dy.shape[-1]), x.reshape(-1, x.shape[-1]))
+        return dx, None, dy, None
+
+
+class _FusedXentFn(torch.autograd.Function):
+    """Mean token cross entropy of fp16/bf16 logits via cs_xent_fwd/bwd; the
+    gradient overwrites the (dead) logits buffer."""
+
+    @staticmethod
+    def forward(ctx, logits: torch.Tensor, targets: torch.Tensor):
+        from . import kernels as K
+        loss_rows, lse = K.xent_fwd(logits, targets)
+        ctx.save_for_backward(logits, targets, lse)
+        return loss_rows.mean()
+
+    @staticmethod
+    def backward(ctx, dloss: torch.Tensor):
+        from . import kernels as K
+        logits, targets, lse = ctx.saved_tensors
+        K.xent_bwd_(logits, targets, lse, dloss, 1.0 / logits.shape[0])
+        return logits, None
+
+
+def fused_cross_entropy(logits: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+    return _FusedXentFn.apply(logits, targets)
+
+
 def write_grad_into_slot(w: nn.Parameter, dy2: torch.Tensor, x2: torch.Tensor) -> None:
     """dW = dy^T x written over the parameter's own chunk slot."""
     torch.mm(dy2.t(), x2, out=w.data)
@@ -128,8 +173,10 @@ def _bracket(marker, driver, ev_fwd, ev_bwd, xs):
 
 class GPTBlock(nn.Module):
     def __init__(self, schema: ModelSchema, layer: int, driver: EventDriver,
-                 dtype: torch.dtype, grad_sink: Callable, placeholders: bool = False):
+                 dtype: torch.dtype, grad_sink: Callable, placeholders: bool = False,
+                 fused: bool = False):
         super().__init__()
+        self.fused = fused
         H = schema.hidden_dim
         self.heads, self.layer, self.driver, self.grad_sink = schema.heads, layer, driver, grad_sink
         shapes = {"qkv": [(H, H)] * 3, "attn_out": [(H, H)], "mlp_in": [(2 * H, H)] * 2,
@@ -145,6 +192,11 @@ class GPTBlock(nn.Module):
 
     def _lin(self, x, w):
         return _ChunkLinearFn.apply(x, w, self.grad_sink)
+
+    def _lin_res(self, x, w, residual):
+        if not self.fused:
+            return residual + self._lin(x, w)
+        return _ChunkLinearResFn.apply(x, w, residual, self.grad_sink)
 
     def _slot(self, name, xs, fn):
         fwd, bwd = self.events[name]
@@ -166,23 +218,23 @@ class GPTBlock(nn.Module):
         o = F.scaled_dot_product_attention(heads(q), heads(k), heads(v), is_causal=True)
         o = o.transpose(1, 2).reshape(B, S, H)
         (wo,) = self.slots["attn_out"]
-        (attn,) = self._slot("attn_out", (o,), lambda x: (self._lin(x, wo),))
-        h = h + attn
+        (h,) = self._slot("attn_out", (o, h), lambda x, r: (self._lin_res(x, wo, r),))
         b = F.layer_norm(h, (H,))
         w1a, w1b = self.slots["mlp_in"]
         u1, u2 = self._slot("mlp_in", (b,), lambda x: (self._lin(x, w1a), self._lin(x, w1b)))
         g1, g2 = F.gelu(u1, approximate="tanh"), F.gelu(u2, approximate="tanh")
         w2a, w2b = self.slots["mlp_out"]
-        (y,) = self._slot("mlp_out", (g1, g2),
-                          lambda x1, x2: (self._lin(x1, w2a) + self._lin(x2, w2b),))
-        return h + y
+        (h,) = self._slot("mlp_out", (g1, g2, h),
+                          lambda x1, x2, r: (self._lin_res(x2, w2b, self._lin_res(x1, w2a, r)),))
+        return h
 
 
 class ReferenceShapedGPT(nn.Module):
     """GPT with tied embedding/LM head; see module docstring."""
 
     def __init__(self, schema: ModelSchema, dtype: torch.dtype = torch.float16,
-                 grad_sink: Callable = write_grad_into_slot, placeholders: bool = False):
+                 grad_sink: Callable = write_grad_into_slot, placeholders: bool = False,
+                 fused: bool = False):
         """``placeholders``: parameters start as empty tensors; their ``.data``
         is bound to chunk slots (or embedding buffers) by the executor."""
         super().__init__()
@@ -191,8 +243,9 @@ class ReferenceShapedGPT(nn.Module):
         V, S, H = schema.vocab, schema.seq_len, schema.hidden_dim
         self.wte = nn.Parameter(torch.empty(0 if placeholders else (V, H), dtype=dtype))
         self.wpe = nn.Parameter(torch.empty(0 if placeholders else (S, H), dtype=dtype))
+        self.fused = fused
         self.blocks = nn.ModuleList([GPTBlock(schema, l, self.driver, dtype, grad_sink,
-                                              placeholders)
+                                              placeholders, fused)
                                      for l in range(schema.layers)])
         self.embedding_events = (-1, -1)
 
@@ -226,6 +279,8 @@ class ReferenceShapedGPT(nn.Module):
             h = blk(h)
         h = F.layer_norm(h, (self.schema.hidden_dim,))
         logits = F.linear(h, self.wte)
+        if self.fused:  # sm_100a fused loss kernels (cs_xent_fwd/bwd)
+            return fused_cross_entropy(logits.view(B * S, -1), targets.reshape(B * S))
         return F.cross_entropy(logits.float().view(B * S, -1), targets.reshape(B * S))
 
 

@@ -220,3 +220,33 @@ def master_init(p32: torch.Tensor, m: torch.Tensor, v: torch.Tensor, src: torch.
                                     ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(src.data_ptr()),
                                     SRC_CODE[src.dtype], int(n), _stream(stream)),
             "cs_master_init")
+
+
+def xent_fwd(logits: torch.Tensor, targets: torch.Tensor,
+             stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """Per-row cross-entropy loss and logsumexp of fp16/bf16 logits [rows, vocab]."""
+    _need_cuda(logits, targets)
+    if logits.dim() != 2 or not logits.is_contiguous() or targets.dtype != torch.int64:
+        raise ValueError("xent_fwd wants contiguous 2-D logits and int64 targets")
+    rows, vocab = logits.shape
+    tg = targets.reshape(-1).contiguous()
+    loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    N.check(N.load().cs_xent_fwd(ctypes.c_void_p(logits.data_ptr()), ctypes.c_void_p(tg.data_ptr()),
+                                 rows, vocab, _code(logits.dtype), ctypes.c_void_p(loss.data_ptr()),
+                                 ctypes.c_void_p(lse.data_ptr()), _stream(stream)), "cs_xent_fwd")
+    return loss, lse
+
+
+def xent_bwd_(logits: torch.Tensor, targets: torch.Tensor, lse: torch.Tensor,
+              dloss: torch.Tensor, scale: float,
+              stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """In place: logits <- (softmax - onehot) * dloss * scale."""
+    rows, vocab = logits.shape
+    tg = targets.reshape(-1).contiguous()
+    d = dloss.reshape(1).float().contiguous()
+    N.check(N.load().cs_xent_bwd(ctypes.c_void_p(logits.data_ptr()), ctypes.c_void_p(tg.data_ptr()),
+                                 ctypes.c_void_p(lse.data_ptr()), ctypes.c_void_p(d.data_ptr()),
+                                 float(scale), rows, vocab, _code(logits.dtype),
+                                 _stream(stream)), "cs_xent_bwd")
+    return logits

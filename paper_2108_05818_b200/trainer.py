@@ -54,7 +54,7 @@ class ChunkTrainer:
                  dynamic_loss_scale: Optional[bool] = None,
                  non_model_fn: Optional[Callable[[int], int]] = None,
                  host_threads: int = 0, time_copies: bool = False,
-                 cuda_graph: bool = False):
+                 cuda_graph: bool = False, fused_ops: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -88,7 +88,8 @@ class ChunkTrainer:
                              non_model_fn=non_model_fn)
         self.nproc, self.rank = nproc, rank
         with torch.device(self.device):
-            self.model = ReferenceShapedGPT(schema, dtype=dtype, placeholders=True)
+            self.model = ReferenceShapedGPT(schema, dtype=dtype, placeholders=True,
+                                            fused=fused_ops)
         self.shapes = reference_tensor_shapes(schema)
         self.model.attach_events(self.sim.timeline)
         self._events = self.sim.timeline.events
