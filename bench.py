@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="eager steps only (no CUDA-graph replay of the steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-offload-probe", action="store_true",
+                    help="skip the host-offload side measurement (chunk moves GB/s)")
     ap.add_argument("--cpu-sample-batch", type=int, default=1)
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
@@ -123,6 +125,85 @@ class ClockSampler:
         med = sm[len(sm) // 2] if sm else None
         return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def host_link_peak(dev, nbytes=1 << 30, iters=5):
+    """Pinned cudaMemcpyAsync bandwidth H2D / D2H (GB/s), CUDA events."""
+    import torch
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    devb = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, dst, src in (("h2d", devb, host), ("d2h", host, devb)):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            dst.copy_(src, non_blocking=True)
+        b_.record()
+        torch.cuda.synchronize()
+        out[name] = nbytes * iters / (a.elapsed_time(b_) * 1e-3) / 1e9
+    return out
+
+
+def offload_probe(schema_kw, dev, steps=3, warmup=2):
+    """The same 1B step with every optimizer triplet in pinned host DRAM
+    (os_placement=cpu): grads D2H + host fused Adam + params H2D as
+    `adam_copy` (`engine.py:249-251, 265-267`).  Reports the chunk moves'
+    achieved host-link GB/s from copy-stream CUDA events."""
+    import torch
+    from paper_2108_05818_b200 import kernels as K
+    from paper_2108_05818_b200.config import PolicySpec
+    from paper_2108_05818_b200.model import build_gpt_schema
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    peak = host_link_peak(dev)
+    schema = build_gpt_schema(**schema_kw)
+    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=64 << 20, os_placement="cpu"),
+                      seed=0, hyper=K.AdamHyper(lr=1e-4), time_copies=True)
+    gen = torch.Generator().manual_seed(7)
+    toks = [torch.randint(0, schema.vocab, (schema.batch, schema.seq_len + 1),
+                          generator=gen).to(dev) for _ in range(2)]
+    for i in range(warmup):
+        tr.step(toks[i % 2])
+    torch.cuda.synchronize()
+    st = tr.executor.stats
+    st.copy_events.clear()
+    host0, items0 = st.host_adam_seconds, st.host_adam_items
+    a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(steps):
+        tr.step(toks[i % 2])
+    b_.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b_) / steps
+    agg = {}
+    for name, nbytes, e0, e1 in st.copy_events:
+        t = e0.elapsed_time(e1)
+        s = agg.setdefault(name, [0, 0.0, 0])
+        s[0] += nbytes
+        s[1] += t
+        s[2] += 1
+    moves = {}
+    for name, (nbytes, t, n) in agg.items():
+        key = "h2d" if name == "cpu>gpu" else "d2h"
+        gbs = nbytes / (t * 1e-3) / 1e9 if t > 0 else None
+        moves[key] = {"copies": n, "bytes": nbytes, "achieved_gbs": round(gbs, 1),
+                      "peak_gbs": round(peak[key], 1), "frac": round(gbs / peak[key], 3)}
+    rep = tr.reports[-1]
+    out = {"workload": "GPT-1B step, os_placement=cpu (every optimizer triplet in pinned host "
+                       "DRAM), B=%d" % schema.batch,
+           "ms_per_step": round(ms, 2),
+           "tokens_per_s": round(schema.batch * schema.seq_len / (ms * 1e-3), 1),
+           "ledger_pcie_bytes_per_step": rep.pcie_bytes,
+           "chunk_moves": moves,
+           "host_adam_s_per_step": round((st.host_adam_seconds - host0) / steps, 4),
+           "host_adam_gelem_per_s": round(
+               sum(tr.sim.chunk_set.param_chunk(p).used_elems for p in tr.sim.local)
+               / max((st.host_adam_seconds - host0) / steps, 1e-9) / 1e9, 3),
+           "prefetch_hits": st.prefetch_hits, "peak_source": "pinned cudaMemcpyAsync 1 GiB"}
+    del tr
+    torch.cuda.empty_cache()
+    return out
 
 
 def cpu_baseline(schema_kw, sample_batch, steps=1):
@@ -318,6 +399,13 @@ def main():
         "clocks": clk,
         "final_loss": final_loss, "loss_scale": st.loss_scale, "adam_steps": int(st.step),
     }
+    if world == 1 and not args.no_offload_probe:
+        del trainer, ex
+        torch.cuda.empty_cache()
+        try:
+            out["offload_probe"] = offload_probe(schema_kw, dev)
+        except Exception as e:  # reported, never fatal
+            out["offload_probe"] = {"error": repr(e)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(schema_kw, args.cpu_sample_batch)

@@ -73,13 +73,17 @@ class IterationReport:
 class StepExecutor:
     """Physical side of the step (no-op base class = accounting only)."""
 
+    def before_event(self, ev, iteration: int) -> None:
+        """Called before any decision of ``ev`` (prefetch hook)."""
+        pass
+
     def on_compute_start(self, ev, chunks: Sequence[Chunk]) -> None:
         pass
 
     def on_compute_finish(self, ev, chunks: Sequence[Chunk]) -> None:
         pass
 
-    def on_adam_begin(self, iteration: int) -> None:
+    def on_adam_begin(self, iteration: int, plan=None) -> None:
         pass
 
     def init_optimizer_state(self, position: int, device: str) -> None:
@@ -283,7 +287,7 @@ class Engine:
         mgr, cs, ex = self.manager, self.chunk_set, self.executor
         staging = ChunkKind.PARAM_FP32.elem_bytes * cs.capacity_elems
         if ex is not None:
-            ex.on_adam_begin(iteration)
+            ex.on_adam_begin(iteration, plan)
         for pos in local_positions:
             device = plan.device_of_position(pos)
             triplet = cs.os_triplet(pos)
@@ -397,6 +401,8 @@ class Engine:
 
     def _start_body(self, ev) -> None:
         it = self._it
+        if self.executor is not None:
+            self.executor.before_event(ev, it.report.iteration)
         m = 2 * ev.index + 1
         self.manager.set_non_model(GPU, self.non_model_fn(m), m)
         if ev.phase is Phase.ADAM:

@@ -32,6 +32,7 @@ allocator (chunk-sized blocks are recycled step to step), host slabs from
 its pinned caching host allocator.
 """
 
+import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Set, Tuple
 
@@ -86,6 +87,11 @@ class ExecStats:
     reduce_scatters: int = 0
     adam_launch_items: int = 0
     host_adam_items: int = 0
+    prefetch_issued: int = 0
+    prefetch_hits: int = 0
+    prefetch_discarded: int = 0
+    prefetch_discarded_bytes: int = 0
+    host_adam_seconds: float = 0.0
     copy_events: List[Tuple[str, int, "torch.cuda.Event", "torch.cuda.Event"]] = field(
         default_factory=list)
 
@@ -117,6 +123,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._group_slab: Dict[int, torch.Tensor] = {}
         self._pending: List[Tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, int]] = []
         self._pending_ids: Set[int] = set()
+        self._prefetched: Dict[int, Tuple[torch.Tensor, "torch.cuda.Event"]] = {}
+        self._predrained: Dict[int, Tuple[torch.Tensor, "torch.cuda.Event"]] = {}
+        self._prefetch_sched: Dict[int, List[int]] = {}
+        self.prefetch_depth = 0
+        self._plan = None
         self._host_state = None
         self._placeholder = torch.empty(0, dtype=dtype, device=self.device)
         self.chunk_set: Optional[ChunkSet] = None
@@ -161,6 +172,16 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                                device=self.device)
         return torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk), pin_memory=True)
 
+    def _alloc_for_copy(self, chunk: Chunk) -> torch.Tensor:
+        """HBM destination of an H2D copy, taken from the copy stream's pool so
+        the copy need not wait for the compute stream; the compute stream is
+        registered as a user (it consumes the payload after `wait_ready`)."""
+        with torch.cuda.stream(self.copy_stream):
+            d = torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk),
+                            device=self.device)
+        d.record_stream(self.compute)
+        return d
+
     def tensor(self, chunk: Chunk, device: str) -> torch.Tensor:
         return self.payload[device][chunk.chunk_id]
 
@@ -190,12 +211,22 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self._flush_adam()  # the move must carry post-update bytes
         if src == GPU and chunk.chunk_id in self._awaiting_gather:
             raise RuntimeError("chunk %d moved before its gather landed" % chunk.chunk_id)
-        s = self.payload[src][chunk.chunk_id]
-        d = self._retained.pop((chunk.chunk_id, dst), None)
-        if d is None:
-            d = self._alloc(chunk, dst)
-        prior = self.ready.pop((chunk.chunk_id, src), None)
-        done = self._transfer(s, d, src, dst, prior)
+        if dst == CPU and chunk.chunk_id in self._prefetched:
+            self._discard_prefetch(chunk)
+        if dst == GPU:
+            hit = self._prefetched.pop(chunk.chunk_id, None)
+        else:
+            hit = self._predrained.pop(chunk.chunk_id, None)
+        if hit is not None:  # issued ahead of time from the previous iteration's ledger
+            d, done = hit
+            self.stats.prefetch_hits += 1
+        else:
+            s = self.payload[src][chunk.chunk_id]
+            d = self._retained.pop((chunk.chunk_id, dst), None)
+            if d is None:
+                d = self._alloc_for_copy(chunk) if dst == GPU else self._alloc(chunk, dst)
+            prior = self.ready.pop((chunk.chunk_id, src), None)
+            done = self._transfer(s, d, src, dst, prior)
         if done is not None:
             self.ready[(chunk.chunk_id, dst)] = done
         self.payload[dst][chunk.chunk_id] = d
@@ -203,9 +234,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     def _transfer(self, s: torch.Tensor, d: torch.Tensor, src: str, dst: str,
                   prior: Optional["torch.cuda.Event"]):
         """cudaMemcpyAsync of a whole payload on the copy stream; returns the
-        completion event consumers wait on (`wait_ready`)."""
+        completion event consumers wait on (`wait_ready`).  D2H waits for the
+        compute stream (the payload must be final); H2D does not (its source
+        is host data already final, its destination came from the copy
+        stream's pool)."""
         cs = self.copy_stream
-        cs.wait_stream(self.compute)   # source final, destination block free
+        if src == GPU:
+            cs.wait_stream(self.compute)
         if prior is not None:
             cs.wait_event(prior)
         with torch.cuda.stream(cs):
@@ -219,13 +254,54 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             s.record_stream(cs)
             self.stats.d2h_bytes += s.numel() * s.element_size()
         if dst == GPU:
-            d.record_stream(cs)
             self.stats.h2d_bytes += d.numel() * d.element_size()
         if t0 is not None:
             self.stats.copy_events.append(("%s>%s" % (src, dst), d.numel() * d.element_size(),
                                            t0, done))
         self.stats.copies += 1
         return done
+
+    # -- prefetch from the previous iteration's ledger (the warm-up trace) ---------
+    #
+    # The schedule reaches a fixed point after warm-up (identical ledgers per
+    # measured iteration), so the fetches of the next events are known before
+    # the accounting takes them.  Before event i, every CPU->GPU fetch the last
+    # iteration made during events i+1 .. i+prefetch_depth is issued on the
+    # copy stream if the chunk's host payload is final (the chunk is not on the
+    # GPU and no host write can intervene before the fetch: prefetches never
+    # cross the ADAM event, and any D2H into / drop of the host copy discards
+    # them).  The accounting fetch then adopts the in-flight buffer.
+
+    def set_prefetch_schedule(self, transfers) -> None:
+        sched: Dict[int, List[int]] = {}
+        for t in transfers:
+            if t.src == CPU and t.dst == GPU and isinstance(t.chunk_id, int):
+                sched.setdefault((t.moment - 1) // 2, []).append(t.chunk_id)
+        self._prefetch_sched = sched
+
+    def before_event(self, ev, iteration: int) -> None:
+        if not self.prefetch_depth or not self._prefetch_sched:
+            return
+        cs = self.chunk_set
+        for j in range(ev.index + 1, ev.index + 1 + self.prefetch_depth):
+            for cid in self._prefetch_sched.get(j, ()):
+                if cid in self._prefetched or cid in self.payload[GPU]:
+                    continue
+                src = self.payload[CPU].get(cid)
+                if src is None:
+                    continue
+                chunk = cs.chunks[cid]
+                d = self._alloc_for_copy(chunk)
+                prior = self.ready.get((cid, CPU))
+                done = self._transfer(src, d, CPU, GPU, prior)
+                self._prefetched[cid] = (d, done)
+                self.stats.prefetch_issued += 1
+
+    def _discard_prefetch(self, chunk: Chunk) -> None:
+        hit = self._prefetched.pop(chunk.chunk_id, None)
+        if hit is not None:
+            self.stats.prefetch_discarded += 1
+            self.stats.prefetch_discarded_bytes += hit[0].numel() * hit[0].element_size()
 
     def materialize(self, chunk: Chunk, device: str) -> None:
         key = (chunk.chunk_id, device)
@@ -238,6 +314,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     def drop(self, chunk: Chunk, device: str) -> None:
         cid = chunk.chunk_id
         key = (cid, device)
+        if device == CPU:
+            self._discard_prefetch(chunk)
         t = self.payload[device].pop(cid, None)
         self._awaiting_gather.discard(cid)
         ev = self.ready.pop(key, None)
@@ -341,9 +419,12 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.params[tid].data = gpu[cid][off:off + n].view(self.shapes[tid])
             self._bound[tid] = cid
 
-    def on_adam_begin(self, iteration: int) -> None:
+    def on_adam_begin(self, iteration: int, plan=None) -> None:
         """Global grad norm / found-inf and the device step scalars."""
         cs = self.chunk_set
+        self._plan = plan
+        for cid in list(self._prefetched):  # prefetches never cross the ADAM event
+            self._discard_prefetch(cs.chunks[cid])
         self._host_state = None
         emb_grads = []
         for param, _, _, _ in self.embedding:
@@ -372,6 +453,19 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.comm.all_reduce_sum(self.state.sumsq())
         K.adam_prepare(self.state, self.hyper, max_grad_norm=self.max_grad_norm,
                        dynamic_scale=self.dynamic_loss_scale)
+        # host-placed positions: drain their gradients D2H now, in walk order,
+        # so host Adam on position k overlaps the copy of position k+1 (the
+        # accounting bills the same rows at each position's turn)
+        plan = self._plan
+        if plan is not None and self.prefetch_depth:
+            for pos in self.partition.local_positions(self.rank):
+                chunk = cs.param_chunk(pos)
+                if plan.device_of_position(pos) == CPU and self.has(chunk, GPU) \
+                        and not self.has(chunk, CPU):
+                    d = self._alloc(chunk, CPU)
+                    done = self._transfer(self.tensor(chunk, GPU), d, GPU, CPU,
+                                          self.ready.get((chunk.chunk_id, GPU)))
+                    self._predrained[chunk.chunk_id] = (d, done)
         # non-chunked embedding: its autograd gradient is packed over the
         # parameter (K3) so it follows the same in-place update as a chunk
         for param, master, m, v in self.embedding:
@@ -407,13 +501,16 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self._pending_ids.update(c.chunk_id for c in (param,) + triplet)
             return
         if self._host_state is None:
+            self._flush_adam()  # device positions update while the host works
             self._host_state = self.state.read()  # one sync per step, only with host positions
         for c in (param,) + triplet:
             self.wait_ready(c, CPU)
         p16 = self.tensor(param, CPU)
         p32, m, v = (self.tensor(c, CPU) for c in triplet)
+        t0 = time.perf_counter()
         K.adam_chunks_host([(p16, p32, m, v, n)], self.hyper, self._host_state,
                            self.host_threads)
+        self.stats.host_adam_seconds += time.perf_counter() - t0
         self.stats.host_adam_items += 1
 
     def retain_param_payload(self, chunk: Chunk, device: str) -> None:
@@ -442,6 +539,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._flush_adam()
         self._retain_req.clear()
         self._retained.clear()
+        self._predrained.clear()
 
     def end_of_warmup(self) -> None:
         """The fp32 init copies read zero-copy by K6 can go once it has run."""

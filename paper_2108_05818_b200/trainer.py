@@ -54,7 +54,8 @@ class ChunkTrainer:
                  dynamic_loss_scale: Optional[bool] = None,
                  non_model_fn: Optional[Callable[[int], int]] = None,
                  host_threads: int = 0, time_copies: bool = False,
-                 cuda_graph: bool = False, fused_ops: bool = True):
+                 cuda_graph: bool = False, fused_ops: bool = True,
+                 prefetch_depth: int = 2):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -107,6 +108,7 @@ class ChunkTrainer:
         self.iteration = 0
         self.reports: List[IterationReport] = []
         self.cuda_graph = cuda_graph
+        self.prefetch_depth = prefetch_depth
         self._graph = None
         self._side = None
         self.graph_kernels_per_step = 0
@@ -202,6 +204,9 @@ class ChunkTrainer:
         self.reports.append(report)
         if warm:
             self.executor.end_of_warmup()
+        else:  # the schedule is at its fixed point: prefetch next iteration's fetches
+            self.executor.prefetch_depth = self.prefetch_depth
+            self.executor.set_prefetch_schedule(report.transfers)
         self.iteration += 1
         return loss.detach()
 

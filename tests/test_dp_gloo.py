@@ -67,6 +67,9 @@ class HostDoubleExecutor(ChunkPayloadExecutor):
     def _alloc(self, chunk, device):
         return torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk))
 
+    def _alloc_for_copy(self, chunk):
+        return self._alloc(chunk, "gpu")
+
     def _transfer(self, s, d, src, dst, prior):
         d.copy_(s)
         self.stats.copies += 1
@@ -82,7 +85,7 @@ class HostDoubleExecutor(ChunkPayloadExecutor):
                 g = _fake_grad(view.numel(), self.rank)
                 view.reshape(-1).copy_(torch.from_numpy(g))
 
-    def on_adam_begin(self, iteration):
+    def on_adam_begin(self, iteration, plan=None):
         self.os_state.sumsq = 1.0
         self.O.adam_prepare(self.os_state, LR, B1, B2)
 

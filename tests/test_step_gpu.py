@@ -72,7 +72,8 @@ def test_real_step_ledgers_match_reference(case):
     chunk_rows = [t for r in tr.reports for t in r.transfers if t.chunk_id != "embedding"]
     h2d = sum(t.bytes for t in chunk_rows if (t.src, t.dst) == ("cpu", "gpu"))
     d2h = sum(t.bytes for t in chunk_rows if (t.src, t.dst) == ("gpu", "cpu"))
-    assert tr.executor.stats.h2d_bytes == h2d and tr.executor.stats.d2h_bytes == d2h
+    st = tr.executor.stats
+    assert st.h2d_bytes - st.prefetch_discarded_bytes == h2d and st.d2h_bytes == d2h
 
 
 def test_adam_inside_real_step_matches_oracle():
@@ -102,6 +103,7 @@ def test_host_placement_and_eviction_do_not_change_numerics():
             runs[case] = (losses, params, tr.executor.stats)
         assert runs["tiny_tight"][2].host_adam_items > 0      # host Adam really ran
         assert runs["tiny_tight"][2].d2h_bytes > 0            # evictions really moved data
+        assert runs["tiny_tight"][2].prefetch_hits > 0        # fetches ran ahead of need
         assert runs["tiny_cap256Ki"][0] == runs["tiny_tight"][0]
         for a, b in zip(runs["tiny_cap256Ki"][1], runs["tiny_tight"][1]):
             assert torch.equal(a.view(torch.int16), b.view(torch.int16))
