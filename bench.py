@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="eager steps only (no CUDA-graph replay of the steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
+    ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-offload-probe", action="store_true",
                     help="skip the host-offload side measurement (chunk moves GB/s)")
     ap.add_argument("--cpu-sample-batch", type=int, default=1)
@@ -272,10 +274,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:  # test hook: several ranks on one GPU (gloo only)
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     schema_kw = dict(layers=args.layers, hidden_dim=args.hidden, heads=args.heads,
                      seq_len=args.seq, vocab=args.vocab, batch=args.batch)
