@@ -151,19 +151,61 @@ class _EmbeddingMark(torch.autograd.Function):
 
 
 class EventDriver:
-    """Forwards marker callbacks to the engine; inert when no engine is attached."""
+    """Forwards marker callbacks to the engine; inert when no engine is attached.
+
+    While a checkpointed layer is recomputed (``recomputing``), the FWD event
+    indices its markers carry are remapped to the layer's RE_FWD events."""
 
     def __init__(self):
         self.on_start: Optional[Callable[[int], None]] = None
         self.on_finish: Optional[Callable[[int], None]] = None
+        self.refwd_of: dict = {}
+        self.recomputing = False
+
+    def _map(self, ev: int) -> int:
+        return self.refwd_of.get(ev, -1) if self.recomputing else ev
 
     def start(self, ev: int) -> None:
+        ev = self._map(ev)
         if self.on_start is not None and ev >= 0:
             self.on_start(ev)
 
     def finish(self, ev: int) -> None:
+        ev = self._map(ev)
         if self.on_finish is not None and ev >= 0:
             self.on_finish(ev)
+
+
+class _LayerCheckpoint(torch.autograd.Function):
+    """Activation checkpointing of one GPT block (`model.py:294-306`).
+
+    Forward runs the block without a graph and keeps only the layer input
+    (the reference's checkpointed activation is this one ``u`` per layer).
+    Backward re-runs the block with the driver in RE_FWD mode — its four
+    RE_FWD events fire, with any ``regather_refwd`` all-gathers — and then
+    back-propagates through the recomputed graph, whose markers fire the
+    layer's BWD events: exactly the checkpointed timeline order."""
+
+    @staticmethod
+    def forward(ctx, block, h_in):
+        ctx.block = block
+        ctx.save_for_backward(h_in)
+        with torch.no_grad():
+            return block(h_in)
+
+    @staticmethod
+    def backward(ctx, dout):
+        (h_in,) = ctx.saved_tensors
+        block = ctx.block
+        h = h_in.detach().requires_grad_(True)
+        block.driver.recomputing = True
+        try:
+            with torch.enable_grad():
+                out = block(h)
+        finally:
+            block.driver.recomputing = False
+        torch.autograd.backward(out, dout)
+        return None, h.grad
 
 
 def _bracket(marker, driver, ev_fwd, ev_bwd, xs):
@@ -244,6 +286,7 @@ class ReferenceShapedGPT(nn.Module):
         self.wte = nn.Parameter(torch.empty(0 if placeholders else (V, H), dtype=dtype))
         self.wpe = nn.Parameter(torch.empty(0 if placeholders else (S, H), dtype=dtype))
         self.fused = fused
+        self.checkpointing = False
         self.blocks = nn.ModuleList([GPTBlock(schema, l, self.driver, dtype, grad_sink,
                                               placeholders, fused)
                                      for l in range(schema.layers)])
@@ -263,11 +306,16 @@ class ReferenceShapedGPT(nn.Module):
     def attach_events(self, timeline) -> None:
         """Map every slot / the embedding to its (FWD, BWD) timeline indices."""
         idx = {ev.name: ev.index for ev in timeline.events}
+        self.driver.refwd_of = {}
         for blk in self.blocks:
             for name, _ in OP_SLOTS:
-                blk.events[name] = (idx["l%d.%s.fwd" % (blk.layer, name)],
-                                    idx["l%d.%s.bwd" % (blk.layer, name)])
+                fwd = idx["l%d.%s.fwd" % (blk.layer, name)]
+                blk.events[name] = (fwd, idx["l%d.%s.bwd" % (blk.layer, name)])
+                refwd = idx.get("l%d.%s.refwd" % (blk.layer, name))
+                if refwd is not None:
+                    self.driver.refwd_of[fwd] = refwd
         self.embedding_events = (idx["embedding.fwd"], idx["embedding.bwd"])
+        self.checkpointing = timeline.checkpointed
 
     def forward(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         B, S = tokens.shape
@@ -276,7 +324,7 @@ class ReferenceShapedGPT(nn.Module):
         h = F.embedding(tokens, self.wte) + self.wpe[:S]
         h = _EmbeddingMark.apply(self.driver, efwd, ebwd, h)
         for blk in self.blocks:
-            h = blk(h)
+            h = _LayerCheckpoint.apply(blk, h) if self.checkpointing else blk(h)
         h = F.layer_norm(h, (self.schema.hidden_dim,))
         logits = F.linear(h, self.wte)
         if self.fused:  # sm_100a fused loss kernels (cs_xent_fwd/bwd)

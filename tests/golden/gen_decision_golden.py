@@ -47,6 +47,11 @@ CASES = [
     ("tiny_p2_ckpt", dict(layers=4, hidden_dim=256, heads=4, seq_len=128, batch=4),
      dict(gpu_count=2, gpu_bytes=180 * 10**9),
      dict(capacity_elems=MI // 4, checkpointing=True), 2, [0, 1], 3),
+    # activation checkpointing on one rank under a tight budget (RE_FWD events)
+    ("tiny_ckpt_tight", dict(layers=4, hidden_dim=256, heads=4, seq_len=128, batch=4,
+                             context_bytes=2 * MI),
+     dict(gpu_count=1, gpu_bytes=14 * MI), dict(capacity_elems=MI // 4, checkpointing=True),
+     1, [0], 3),
     # C2 1B on one B200, chunk-size sweep
     ("gpt1b_cap32Mi", dict(layers=20, hidden_dim=2048, heads=16, seq_len=1024, batch=16),
      dict(gpu_count=1, gpu_bytes=180 * 10**9), dict(capacity_elems=32 * MI), 1, [0], 3),

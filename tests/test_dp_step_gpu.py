@@ -68,7 +68,8 @@ def _worker(rank, world, port, outdir, case):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,world", [("tiny_p2", 2), ("tiny_p4_tight", 4), ("tiny_p8", 8)])
+@pytest.mark.parametrize("case,world", [("tiny_p2", 2), ("tiny_p4_tight", 4), ("tiny_p8", 8),
+                                        ("tiny_p2_ckpt", 2)])
 def test_multi_rank_zero_step_on_one_gpu(case, world):
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(world, 29800 + world + os.getpid() % 100, d, case),

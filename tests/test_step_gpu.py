@@ -53,7 +53,8 @@ def _ledger(r):
                         for s in r.samples]}
 
 
-@pytest.mark.parametrize("case", ["tiny_cap1Mi", "tiny_cap256Ki", "tiny_tight", "tiny_os_cpu"])
+@pytest.mark.parametrize("case", ["tiny_cap1Mi", "tiny_cap256Ki", "tiny_tight", "tiny_os_cpu",
+                                  "tiny_ckpt_tight"])
 def test_real_step_ledgers_match_reference(case):
     tr, schema = _trainer(case)
     ref = CASES[case]["ranks"]["0"]
@@ -141,3 +142,23 @@ def test_cuda_graph_replay_matches_eager_steps():
     for r in out[True][2].reports[2:]:
         assert _ledger(r)["transfers"] == ref["transfers"]
         assert _ledger(r)["samples"] == ref["samples"]
+
+
+def test_checkpointing_does_not_change_numerics():
+    """Recomputed activations give bit-identical training (deterministic attention)."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_cap256Ki"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 3)
+    out = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for ckpt in (False, True):
+            pol = dict(c["policy"], checkpointing=ckpt)
+            tr = ChunkTrainer(schema, PolicySpec(**pol), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0)
+            out[ckpt] = [tr.step_host(t) for t in toks]
+            if ckpt:
+                names = [tr.sim.timeline.events[0].name]
+                assert tr.sim.timeline.checkpointed and tr.model.checkpointing
+    assert out[True] == out[False]
