@@ -287,6 +287,13 @@ class ChunkTrainer:
 
     # -- inspection -----------------------------------------------------------------------------
 
+    def write_ledgers(self, out_dir: str) -> List[str]:
+        """The real run's layout / moments / transfers / collectives CSVs and
+        summary in the reference's wire format (:mod:`.ledgers`)."""
+        from . import ledgers
+        return ledgers.write_ledgers(out_dir, self.reports, self.sim.chunk_set.layout_rows(),
+                                     self.sim.engine.plan)
+
     def step_state(self):
         return self.executor.state.read()
 

@@ -162,3 +162,17 @@ def test_checkpointing_does_not_change_numerics():
                 names = [tr.sim.timeline.events[0].name]
                 assert tr.sim.timeline.checkpointed and tr.model.checkpointing
     assert out[True] == out[False]
+
+
+def test_real_run_ledger_files_equal_reference_files(tmp_path):
+    """A real B200 run writes the same ledger bytes the reference simulator
+    writes for the same config (tests/golden/ledgers/tiny_tight)."""
+    tr, schema = _trainer("tiny_tight")
+    for t in _tokens(schema, 3):
+        tr.step_host(t)
+    tr.write_ledgers(str(tmp_path))
+    gold = os.path.join(os.path.dirname(__file__), "golden", "ledgers", "tiny_tight")
+    for fname in ("layout.csv", "moments_chunk.csv", "transfers_chunk.csv",
+                  "collectives_chunk.csv"):
+        with open(os.path.join(gold, fname), "rb") as f, open(tmp_path / fname, "rb") as g:
+            assert g.read() == f.read(), fname
