@@ -55,7 +55,7 @@ class ChunkTrainer:
                  non_model_fn: Optional[Callable[[int], int]] = None,
                  host_threads: int = 0, time_copies: bool = False,
                  cuda_graph: bool = False, fused_ops: bool = True,
-                 prefetch_depth: int = 2):
+                 prefetch_depth: int = 2, non_model: str = "analytic"):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -84,6 +84,12 @@ class ChunkTrainer:
             dynamic_loss_scale=dynamic_loss_scale, max_grad_norm=max_grad_norm, comm=comm,
             host_threads=host_threads, time_copies=time_copies)
         ex = self.executor
+        self.tracer = None
+        if non_model == "measured" and non_model_fn is None:
+            from .tracer import MemoryTracer
+            self.tracer = non_model_fn = MemoryTracer(ex, self.device)
+        elif non_model not in ("analytic", "measured"):
+            raise ValueError("non_model must be 'analytic' or 'measured'")
         self.sim = Simulator(schema, hardware, self.policy, nproc=nproc, rank=rank,
                              payload_backend=ex, collective_backend=ex, executor=ex,
                              non_model_fn=non_model_fn)
@@ -155,7 +161,7 @@ class ChunkTrainer:
         if self.sim.engine.iteration_failed:
             r = self.sim.engine._it.report
             raise OOMError("gpu" if r.failure_reason == "GPU_OOM" else "cpu",
-                           r.failure_moment or -1, 0, 0)
+                           -1 if r.failure_moment is None else r.failure_moment, 0, 0)
 
     def _on_start(self, idx: int) -> None:
         self.sim.engine.start_event(self._events[idx])
@@ -204,6 +210,8 @@ class ChunkTrainer:
         self.reports.append(report)
         if warm:
             self.executor.end_of_warmup()
+            if self.tracer is not None:
+                self.tracer.freeze()
         else:  # the schedule is at its fixed point: prefetch next iteration's fetches
             self.executor.prefetch_depth = self.prefetch_depth
             self.executor.set_prefetch_schedule(report.transfers)

@@ -1,1 +1,1 @@
-python -m pytest tests/test_step_gpu.py tests/test_dp_step_gpu.py -q -x 2>&1 | tail -6
+python -m pytest tests/test_step_gpu.py -q -x 2>&1 | tail -8

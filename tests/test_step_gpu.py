@@ -176,3 +176,46 @@ def test_real_run_ledger_files_equal_reference_files(tmp_path):
                   "collectives_chunk.csv"):
         with open(os.path.join(gold, fname), "rb") as f, open(tmp_path / fname, "rb") as g:
             assert g.read() == f.read(), fname
+
+
+def test_measured_warmup_tracer_drives_the_same_decisions():
+    """non_model='measured': the warm-up's live R - C readings drive the plan
+    and the frozen curve drives later iterations; replaying exactly those
+    values through the accounting-only engine (pinned to the reference by
+    tests/test_decisions_golden.py) reproduces every ledger row."""
+    from paper_2108_05818_b200.scenario import Simulator
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_tight"]
+    schema = build_gpt_schema(**c["schema"])
+    probe = ChunkTrainer(schema, PolicySpec(**c["policy"]),
+                         HardwareSpec(gpu_count=1, gpu_bytes=8 << 30), dtype=torch.float16,
+                         seed=0, non_model="measured")
+    probe.step_host(_tokens(schema, 1)[0])
+    budget = probe.tracer.peak + (24 << 20)  # measured footprint + a few chunks
+    del probe
+    import gc
+    gc.collect()
+    hw = HardwareSpec(gpu_count=1, gpu_bytes=budget)
+    tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), hw, dtype=torch.float16, seed=0,
+                      non_model="measured")
+    for t in _tokens(schema, 3):
+        tr.step_host(t)
+    tracer = tr.tracer
+    assert tracer.frozen and tracer.peak > 0
+    n_moments = tr.sim.timeline.moment_count
+    # the plan's peak = measured R - C plus the accounted BWD staging temp
+    assert tr.sim.engine.plan.peak_non_model_bytes >= max(v for _, v in
+                                                          tracer.history[:n_moments])
+    assert any(t.reason in ("evict", "adam_copy") for r in tr.reports for t in r.transfers)
+    values = list(tracer.history)
+
+    def replay(m):
+        mm, v = values.pop(0)
+        assert mm == m
+        return v
+
+    sim = Simulator(schema, hw, PolicySpec(**c["policy"]), non_model_fn=replay)
+    run = sim.run(3)
+    assert not values
+    for mine, ref in zip(tr.reports, run.reports):
+        assert _ledger(mine) == _ledger(ref)
