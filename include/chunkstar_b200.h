@@ -119,6 +119,13 @@ int         cs_num_sms(void);
 int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
                    const CsAdamHyper* hyper, const CsStepState* d_state,
                    void* stream);
+/* Tuning: select K1's data-movement variant (bit-identical results):
+ * 0-4 SIMT register-tiled (groups/thread x min CTAs/SM), 5-7 TMA-staged
+ * (cp.async.bulk + mbarrier ring; 5: 2048x4 stages, 6: 2048x3 at 2 CTAs/SM,
+ * 7: 4096x3; 8-10 add a dedicated bulk-store warp: 2048x6, 2048x3 at
+ * 2 CTAs/SM, 1024x4 at 3 CTAs/SM).  v < 0 only queries.  Default from
+ * $CS_ADAM_VARIANT, else 0. */
+int cs_adam_variant(int v);
 
 /* ---- K2: gradient sum of squares -------------------------------------------
  * Global grad-norm / found-inf for clipping and dynamic loss scaling (no

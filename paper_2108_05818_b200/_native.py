@@ -52,6 +52,7 @@ SIGNATURES = {
                                       ctypes.POINTER(CsAdamHyper), ctypes.c_void_p,
                                       ctypes.c_void_p]),
     "cs_sumsq_partials": (ctypes.c_int, []),
+    "cs_adam_variant": (ctypes.c_int, [ctypes.c_int]),
     "cs_grad_sumsq": (ctypes.c_int, [ctypes.POINTER(CsGradItem), ctypes.c_int, ctypes.c_int,
                                      ctypes.c_void_p, ctypes.c_void_p]),
     "cs_sumsq_finalize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,

@@ -38,7 +38,9 @@ constexpr int kBlockTile = kThreads * kGroups * 4;
 // every variant computes bit-identical results.
 struct AdamVariant { int groups, min_blocks; };
 constexpr AdamVariant kAdamVariants[] = {{4, 1}, {4, 4}, {2, 4}, {2, 6}, {8, 2}};
-constexpr int kAdamDefault = 0;
+constexpr int kAdamSimtVariants = 5;   // 5..7 = TMA-staged variants (adam_tma.cu)
+constexpr int kAdamVariantCount = 16;
+constexpr int kAdamDefault = 12;  // TMA-staged, 16 consumer warps, 4096 x 3 stages
 
 struct AdamBatch {
   CsAdamItem item[cs::kMaxBatch];
@@ -333,8 +335,7 @@ int adam_variant() {
   if (g_adam_variant < 0) {
     const char* e = getenv("CS_ADAM_VARIANT");
     const int v = e ? atoi(e) : kAdamDefault;
-    g_adam_variant = (v >= 0 && v < (int)(sizeof(kAdamVariants) / sizeof(kAdamVariants[0])))
-                         ? v : kAdamDefault;
+    g_adam_variant = (v >= 0 && v < kAdamVariantCount) ? v : kAdamDefault;
   }
   return g_adam_variant;
 }
@@ -361,7 +362,18 @@ int launch_error(const char* what) {
 
 }  // namespace
 
+int cs_adam_chunks_tma(const CsAdamItem* items, int n_items, int dtype, const CsAdamHyper* h,
+                       const CsStepState* d_state, void* stream, int variant);
+
 extern "C" int cs_num_sms(void) { return num_sms(); }
+
+extern "C" int cs_adam_variant(int v) {
+  if (v >= 0 && v < kAdamVariantCount && v != adam_variant()) {
+    g_adam_variant = v;
+    g_adam_blocks_per_sm = 0;  // occupancy is per kernel
+  }
+  return adam_variant();
+}
 
 extern "C" int cs_sumsq_partials(void) {
   const int sms = num_sms();
@@ -381,7 +393,24 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
     cs::set_error("cs_adam_chunks: no CUDA device");
     return CS_EINVAL;
   }
-  const int variant = adam_variant();
+  int variant = adam_variant();
+  if (variant >= kAdamSimtVariants) {
+    bool ok16 = true;
+    for (int i = 0; i < n_items && ok16; ++i)
+      ok16 = aligned(items[i].p16, 16) && aligned(items[i].p32, 16) && aligned(items[i].m, 16) &&
+             aligned(items[i].v, 16);
+    if (ok16) {
+      for (int i = 0; i < n_items; ++i) {
+        const CsAdamItem& it = items[i];
+        if (it.n < 0 || (it.n > 0 && (!it.p16 || !it.p32 || !it.m || !it.v))) {
+          cs::set_error("cs_adam_chunks: item %d invalid", i);
+          return CS_EINVAL;
+        }
+      }
+      return cs_adam_chunks_tma(items, n_items, dtype, hyper, d_state, stream, variant);
+    }
+    variant = kAdamDefault;  // bulk copies need 16-byte aligned streams
+  }
   const int64_t tile_elems = (int64_t)kThreads * kAdamVariants[variant].groups * 4;
   AdamKernel kern = dtype == CS_FP16 ? adam_kernel_for<CS_FP16>(variant)
                                      : adam_kernel_for<CS_BF16>(variant);

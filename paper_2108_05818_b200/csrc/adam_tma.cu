@@ -1,0 +1,467 @@
+// K1 fused chunk Adam, TMA-staged variant (sm_100a).
+//
+// Same arithmetic as adam_chunks_kernel (adam.cu, bit-identical results);
+// different data movement.  A persistent CTA per SM runs a STAGES-deep ring
+// of shared-memory tiles:
+//
+//   producer (one lane)   : wait empty[s] -> mbarrier expect_tx(14·T bytes) ->
+//                           cp.async.bulk global->shared of the tile's g16,
+//                           p32, m, v (4 bulk copies, complete_tx on full[s])
+//   consumers (8 warps)   : wait full[s] -> Adam in shared memory, in place
+//                           (p16 written over the g16 slot) -> named barrier ->
+//                           one lane: fence.proxy.async, cp.async.bulk
+//                           shared->global of p16, p32, m, v, commit, wait
+//                           until the bulk reads of the stage are done ->
+//                           arrive empty[s]
+//
+// Loads for STAGES tiles are always in flight while the consumers compute and
+// the stores drain asynchronously, so the SM keeps ~STAGES·28 KB of read
+// traffic outstanding with a handful of registers.  Tiles are T elements of
+// one item (the used prefix of one chunk position); each item's last n % 8
+// elements (bulk copies move multiples of 16 B) are updated by the consumer
+// warps straight from global memory.
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "cs_internal.h"
+
+namespace cs_tma {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kThreads = kConsumers + 32;  // + one producer warp
+
+struct Batch {
+  CsAdamItem item[cs::kMaxBatch];
+  int64_t tile_start[cs::kMaxBatch + 1];
+  int n;
+  float b2, c1, c2, eps, wd, decay;
+  int adamw;
+};
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(saddr(src)), "r"(bytes)
+               : "memory");
+}
+
+template <int DT>
+__device__ __forceinline__ float to_f(uint16_t h) {
+  if (DT == CS_FP16) return __half2float(__ushort_as_half(h));
+  return __bfloat162float(__ushort_as_bfloat16(h));
+}
+template <int DT>
+__device__ __forceinline__ uint16_t from_f(float f) {
+  if (DT == CS_FP16) return __half_as_ushort(__float2half_rn(f));
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+struct Consts {
+  float gs, nss, sb, b2, c1, c2, eps, wd, decay;
+  bool adamw;
+};
+
+// identical op sequence to adam.cu's adam1 (torch.optim.Adam association)
+__device__ __forceinline__ void adam1(float g16, float& p, float& m, float& v, const Consts& c) {
+  float g = __fmul_rn(g16, c.gs);
+  if (c.wd != 0.0f) {
+    if (c.adamw) p = __fmul_rn(p, c.decay);
+    else g = __fmaf_rn(c.wd, p, g);
+  }
+  m = __fmaf_rn(c.c1, __fsub_rn(g, m), m);
+  v = __fmaf_rn(__fmul_rn(c.c2, g), g, __fmul_rn(v, c.b2));
+  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.sb), c.eps);
+  p = __fadd_rn(p, __fdiv_rn(__fmul_rn(c.nss, m), denom));
+}
+
+__device__ __forceinline__ int find_item(const int64_t* start, int n, int64_t tile) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (start[mid] <= tile) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int DT, int T, int STAGES>
+__global__ void __launch_bounds__(kThreads)
+adam_tma_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict__ st) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kStageBytes = T * 14;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (st->skip) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = b.tile_start[b.n];
+
+  if (warp == kConsumerWarps) {  // ---- producer warp
+    if (lane == 0) {
+      int64_t k = 0;
+      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++k) {
+        const int s = (int)(k % STAGES);
+        const uint32_t phase = (uint32_t)((k / STAGES) & 1);
+        mbar_wait(&empty[s], phase ^ 1u);
+        const int i = find_item(b.tile_start, b.n, tile);
+        const CsAdamItem it = b.item[i];
+        const int64_t e0 = (tile - b.tile_start[i]) * T;
+        const int64_t nvec = it.n & ~(int64_t)7;
+        const int len = (int)((nvec - e0) < T ? (nvec - e0) : T);
+        unsigned char* base = smem + s * kStageBytes;
+        mbar_expect_tx(&full[s], (uint32_t)len * 14u);
+        bulk_load(base, static_cast<const uint16_t*>(it.p16) + e0, len * 2, &full[s]);
+        bulk_load(base + T * 2, it.p32 + e0, len * 4, &full[s]);
+        bulk_load(base + T * 6, it.m + e0, len * 4, &full[s]);
+        bulk_load(base + T * 10, it.v + e0, len * 4, &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  Consts c;
+  c.gs = st->grad_scale;
+  c.nss = -st->step_size;
+  c.sb = st->sqrt_bc2;
+  c.b2 = b.b2;
+  c.c1 = b.c1;
+  c.c2 = b.c2;
+  c.eps = b.eps;
+  c.wd = b.wd;
+  c.decay = b.decay;
+  c.adamw = b.adamw != 0;
+  const int t = threadIdx.x;
+  int64_t k = 0;
+  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++k) {
+    const int s = (int)(k % STAGES);
+    const uint32_t phase = (uint32_t)((k / STAGES) & 1);
+    const int i = find_item(b.tile_start, b.n, tile);
+    const CsAdamItem it = b.item[i];
+    const int64_t e0 = (tile - b.tile_start[i]) * T;
+    const int64_t nvec = it.n & ~(int64_t)7;
+    const int len = (int)((nvec - e0) < T ? (nvec - e0) : T);
+    unsigned char* base = smem + s * kStageBytes;
+    uint16_t* g16 = reinterpret_cast<uint16_t*>(base);
+    float* p = reinterpret_cast<float*>(base + T * 2);
+    float* m = reinterpret_cast<float*>(base + T * 6);
+    float* v = reinterpret_cast<float*>(base + T * 10);
+    mbar_wait(&full[s], phase);
+    for (int e = t * 4; e < len; e += kConsumers * 4) {
+      uint2 gw = *reinterpret_cast<uint2*>(g16 + e);
+      float4 pp = *reinterpret_cast<float4*>(p + e);
+      float4 mm = *reinterpret_cast<float4*>(m + e);
+      float4 vv = *reinterpret_cast<float4*>(v + e);
+      adam1(to_f<DT>(gw.x & 0xffff), pp.x, mm.x, vv.x, c);
+      adam1(to_f<DT>(gw.x >> 16), pp.y, mm.y, vv.y, c);
+      adam1(to_f<DT>(gw.y & 0xffff), pp.z, mm.z, vv.z, c);
+      adam1(to_f<DT>(gw.y >> 16), pp.w, mm.w, vv.w, c);
+      *reinterpret_cast<float4*>(p + e) = pp;
+      *reinterpret_cast<float4*>(m + e) = mm;
+      *reinterpret_cast<float4*>(v + e) = vv;
+      gw.x = (uint32_t)from_f<DT>(pp.x) | ((uint32_t)from_f<DT>(pp.y) << 16);
+      gw.y = (uint32_t)from_f<DT>(pp.z) | ((uint32_t)from_f<DT>(pp.w) << 16);
+      *reinterpret_cast<uint2*>(g16 + e) = gw;
+    }
+    // make this thread's shared-memory writes visible to the async (bulk copy) proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+    if (t == 0) {
+      bulk_store(static_cast<uint16_t*>(it.p16) + e0, g16, len * 2);
+      bulk_store(it.p32 + e0, p, len * 4);
+      bulk_store(it.m + e0, m, len * 4);
+      bulk_store(it.v + e0, v, len * 4);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      mbar_arrive(&empty[s]);
+    }
+  }
+  // ragged tails (n % 8 elements per item), straight from global memory
+  for (int i = blockIdx.x; i < b.n; i += gridDim.x) {
+    const CsAdamItem it = b.item[i];
+    const int64_t e = (it.n & ~(int64_t)7) + t;
+    if (t < 8 && e < it.n) {
+      uint16_t* q16 = static_cast<uint16_t*>(it.p16);
+      float pp = it.p32[e], mm = it.m[e], vv = it.v[e];
+      adam1(to_f<DT>(q16[e]), pp, mm, vv, c);
+      it.p32[e] = pp;
+      it.m[e] = mm;
+      it.v[e] = vv;
+      q16[e] = from_f<DT>(pp);
+    }
+  }
+  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Three-role variant: producer warp (bulk loads), 8 consumer warps (math),
+// store warp (bulk stores).  Consumers publish a finished stage by arriving on
+// computed[s] (count = all consumer threads) and move straight on; only the
+// store warp waits for the bulk reads before freeing the stage.
+template <int DT, int T, int STAGES, int CW>
+__global__ void __launch_bounds__(CW * 32 + 64)
+adam_tma3_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict__ st) {
+  constexpr int kConsumerWarps = CW;
+  constexpr int kConsumers = CW * 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kStageBytes = T * 14;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* computed = empty + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (st->skip) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&computed[s], kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = b.tile_start[b.n];
+  if (warp >= kConsumerWarps) {
+    if (lane != 0) return;
+    const bool producer = warp == kConsumerWarps;
+    int64_t k = 0;
+    for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++k) {
+      const int s = (int)(k % STAGES);
+      const uint32_t phase = (uint32_t)((k / STAGES) & 1);
+      const int i = find_item(b.tile_start, b.n, tile);
+      const CsAdamItem it = b.item[i];
+      const int64_t e0 = (tile - b.tile_start[i]) * T;
+      const int64_t nvec = it.n & ~(int64_t)7;
+      const int len = (int)((nvec - e0) < T ? (nvec - e0) : T);
+      unsigned char* base = smem + s * kStageBytes;
+      if (producer) {
+        mbar_wait(&empty[s], phase ^ 1u);
+        mbar_expect_tx(&full[s], (uint32_t)len * 14u);
+        bulk_load(base, static_cast<const uint16_t*>(it.p16) + e0, len * 2, &full[s]);
+        bulk_load(base + T * 2, it.p32 + e0, len * 4, &full[s]);
+        bulk_load(base + T * 6, it.m + e0, len * 4, &full[s]);
+        bulk_load(base + T * 10, it.v + e0, len * 4, &full[s]);
+      } else {
+        mbar_wait(&computed[s], phase);
+        bulk_store(static_cast<uint16_t*>(it.p16) + e0, base, len * 2);
+        bulk_store(it.p32 + e0, base + T * 2, len * 4);
+        bulk_store(it.m + e0, base + T * 6, len * 4);
+        bulk_store(it.v + e0, base + T * 10, len * 4);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        // keep this stage's stores in flight; the previous stage's are read
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (k > 0) mbar_arrive(&empty[(int)((k - 1) % STAGES)]);
+      }
+    }
+    if (!producer) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      if (k > 0) mbar_arrive(&empty[(int)((k - 1) % STAGES)]);
+    }
+    return;
+  }
+  Consts c;
+  c.gs = st->grad_scale;
+  c.nss = -st->step_size;
+  c.sb = st->sqrt_bc2;
+  c.b2 = b.b2;
+  c.c1 = b.c1;
+  c.c2 = b.c2;
+  c.eps = b.eps;
+  c.wd = b.wd;
+  c.decay = b.decay;
+  c.adamw = b.adamw != 0;
+  const int t = threadIdx.x;
+  int64_t k = 0;
+  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++k) {
+    const int s = (int)(k % STAGES);
+    const uint32_t phase = (uint32_t)((k / STAGES) & 1);
+    const int i = find_item(b.tile_start, b.n, tile);
+    const int64_t e0 = (tile - b.tile_start[i]) * T;
+    const int64_t nvec = b.item[i].n & ~(int64_t)7;
+    const int len = (int)((nvec - e0) < T ? (nvec - e0) : T);
+    unsigned char* base = smem + s * kStageBytes;
+    uint16_t* g16 = reinterpret_cast<uint16_t*>(base);
+    float* p = reinterpret_cast<float*>(base + T * 2);
+    float* m = reinterpret_cast<float*>(base + T * 6);
+    float* v = reinterpret_cast<float*>(base + T * 10);
+    mbar_wait(&full[s], phase);
+    for (int e = t * 4; e < len; e += kConsumers * 4) {
+      uint2 gw = *reinterpret_cast<uint2*>(g16 + e);
+      float4 pp = *reinterpret_cast<float4*>(p + e);
+      float4 mm = *reinterpret_cast<float4*>(m + e);
+      float4 vv = *reinterpret_cast<float4*>(v + e);
+      adam1(to_f<DT>(gw.x & 0xffff), pp.x, mm.x, vv.x, c);
+      adam1(to_f<DT>(gw.x >> 16), pp.y, mm.y, vv.y, c);
+      adam1(to_f<DT>(gw.y & 0xffff), pp.z, mm.z, vv.z, c);
+      adam1(to_f<DT>(gw.y >> 16), pp.w, mm.w, vv.w, c);
+      *reinterpret_cast<float4*>(p + e) = pp;
+      *reinterpret_cast<float4*>(m + e) = mm;
+      *reinterpret_cast<float4*>(v + e) = vv;
+      gw.x = (uint32_t)from_f<DT>(pp.x) | ((uint32_t)from_f<DT>(pp.y) << 16);
+      gw.y = (uint32_t)from_f<DT>(pp.z) | ((uint32_t)from_f<DT>(pp.w) << 16);
+      *reinterpret_cast<uint2*>(g16 + e) = gw;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(&computed[s]);
+  }
+  for (int i = blockIdx.x; i < b.n; i += gridDim.x) {
+    const CsAdamItem it = b.item[i];
+    const int64_t e = (it.n & ~(int64_t)7) + t;
+    if (t < 8 && e < it.n) {
+      uint16_t* q16 = static_cast<uint16_t*>(it.p16);
+      float pp = it.p32[e], mm = it.m[e], vv = it.v[e];
+      adam1(to_f<DT>(q16[e]), pp, mm, vv, c);
+      it.p32[e] = pp;
+      it.m[e] = mm;
+      it.v[e] = vv;
+      q16[e] = from_f<DT>(pp);
+    }
+  }
+}
+
+template <int DT, int T, int STAGES, bool THREE = false, int CW = 8>
+int launch(const CsAdamItem* items, int n_items, const CsAdamHyper* h,
+           const CsStepState* d_state, cudaStream_t stream, int ctas_per_sm) {
+  constexpr int kSmem = STAGES * T * 14 + 3 * STAGES * 8;
+  static bool configured = false;
+  if (!configured) {
+    if (THREE)
+      cudaFuncSetAttribute(adam_tma3_kernel<DT, T, STAGES, CW>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    else
+      cudaFuncSetAttribute(adam_tma_kernel<DT, T, STAGES>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    configured = true;
+  }
+  const int sms = cs_num_sms();
+  for (int first = 0; first < n_items; first += cs::kMaxBatch) {
+    Batch b;
+    b.n = 0;
+    int64_t tiles = 0;
+    for (int i = first; i < n_items && b.n < cs::kMaxBatch; ++i) {
+      const CsAdamItem& it = items[i];
+      if (it.n == 0) continue;
+      b.item[b.n] = it;
+      b.tile_start[b.n] = tiles;
+      tiles += ((it.n & ~(int64_t)7) + T - 1) / T;
+      ++b.n;
+    }
+    b.tile_start[b.n] = tiles;
+    if (b.n == 0) continue;
+    b.b2 = (float)h->beta2;
+    b.c1 = (float)(1.0 - h->beta1);
+    b.c2 = (float)(1.0 - h->beta2);
+    b.eps = (float)h->eps;
+    b.wd = (float)h->weight_decay;
+    b.decay = (float)(1.0 - h->lr * h->weight_decay);
+    b.adamw = h->adamw;
+    int64_t grid = (int64_t)sms * ctas_per_sm;
+    const int64_t need = tiles > b.n ? tiles : b.n;  // every item's tail needs a CTA
+    if (grid > need) grid = need;
+    if (THREE)
+      adam_tma3_kernel<DT, T, STAGES, CW><<<(int)grid, CW * 32 + 64, kSmem, stream>>>(b, d_state);
+    else
+      adam_tma_kernel<DT, T, STAGES><<<(int)grid, kThreads, kSmem, stream>>>(b, d_state);
+    cs::note_launches(1);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cs::set_error("cs_adam_chunks(tma): launch failed: %s", cudaGetErrorString(e));
+      return (int)e;
+    }
+  }
+  return 0;
+}
+
+}  // namespace cs_tma
+
+// Entry used by cs_adam_chunks for the TMA variants (see adam.cu).
+int cs_adam_chunks_tma(const CsAdamItem* items, int n_items, int dtype, const CsAdamHyper* h,
+                       const CsStepState* d_state, void* stream, int variant) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // variant 5: T=2048 x 4 stages (112 KB), 1 CTA/SM; 6: T=2048 x 3 (84 KB), 2 CTAs/SM;
+  // 7: T=4096 x 3 (168 KB), 1 CTA/SM; three-role: 8: T=2048 x 6 (168 KB) 1 CTA/SM,
+  // 9: T=2048 x 3, 2 CTAs/SM; 10: T=1024 x 4 (57 KB), 3 CTAs/SM
+  if (variant == 11) {  // 16 consumer warps, 2048 x 6 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 12) {  // 16 consumer warps, 4096 x 3 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 4096, 3, true, 16>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 4096, 3, true, 16>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 15) {  // 12 consumer warps, 2048 x 6 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 2048, 6, true, 12>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 2048, 6, true, 12>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 14) {  // 16 consumer warps, 2048 x 7 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 2048, 7, true, 16>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 2048, 7, true, 16>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 13) {  // 12 consumer warps, 2048 x 3 stages, 2 CTAs/SM
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 2048, 3, true, 12>(items, n_items, h, d_state, s, 2);
+    return cs_tma::launch<CS_BF16, 2048, 3, true, 12>(items, n_items, h, d_state, s, 2);
+  }
+  if (variant >= 8) {
+    if (dtype == CS_FP16) {
+      if (variant == 8) return cs_tma::launch<CS_FP16, 2048, 6, true>(items, n_items, h, d_state, s, 1);
+      if (variant == 9) return cs_tma::launch<CS_FP16, 2048, 3, true>(items, n_items, h, d_state, s, 2);
+      return cs_tma::launch<CS_FP16, 1024, 4, true>(items, n_items, h, d_state, s, 3);
+    }
+    if (variant == 8) return cs_tma::launch<CS_BF16, 2048, 6, true>(items, n_items, h, d_state, s, 1);
+    if (variant == 9) return cs_tma::launch<CS_BF16, 2048, 3, true>(items, n_items, h, d_state, s, 2);
+    return cs_tma::launch<CS_BF16, 1024, 4, true>(items, n_items, h, d_state, s, 3);
+  }
+  if (dtype == CS_FP16) {
+    if (variant == 6) return cs_tma::launch<CS_FP16, 2048, 3>(items, n_items, h, d_state, s, 2);
+    if (variant == 7) return cs_tma::launch<CS_FP16, 4096, 3>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_FP16, 2048, 4>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 6) return cs_tma::launch<CS_BF16, 2048, 3>(items, n_items, h, d_state, s, 2);
+  if (variant == 7) return cs_tma::launch<CS_BF16, 4096, 3>(items, n_items, h, d_state, s, 1);
+  return cs_tma::launch<CS_BF16, 2048, 4>(items, n_items, h, d_state, s, 1);
+}

@@ -88,7 +88,21 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="20,22,24,26,28,30")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--adam-variants", default="",
+                    help="comma list of cs_adam_variant ids: time K1 for each")
     args = ap.parse_args()
+    if args.adam_variants:
+        from . import _native as N
+        peak = measured_peak_gbs()
+        for v in [int(x) for x in args.adam_variants.split(",")]:
+            N.load().cs_adam_variant(v)
+            for lg in [int(s) for s in args.sizes.split(",")]:
+                n = 1 << lg
+                ms = bench_size(n, args.iters)["adam"]
+                gbs = 28 * n / (ms * 1e-3) / 1e9
+                print(json.dumps({"kernel": "adam", "variant": v, "n": n, "ms": round(ms, 5),
+                                  "gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4)}))
+        return
     rows = run([int(s) for s in args.sizes.split(",")], args.iters)
     for r in rows:
         print(json.dumps(r))

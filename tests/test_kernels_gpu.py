@@ -34,9 +34,18 @@ def _oracle_state(O, st: "K.N.CsStepState"):
     return s
 
 
+@pytest.fixture(params=[0, 2, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15], ids=lambda v: "variant%d" % v)
+def adam_variant(request, native_lib):
+    old = native_lib.cs_adam_variant(-1)
+    native_lib.cs_adam_variant(request.param)
+    assert native_lib.cs_adam_variant(-1) == request.param
+    yield request.param
+    native_lib.cs_adam_variant(old)
+
+
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("wd,adamw", [(0.0, False), (0.1, False), (0.01, True)])
-def test_adam_chunks_bit_exact(native_lib, oracle_lib, dtype, wd, adamw):
+def test_adam_chunks_bit_exact(native_lib, oracle_lib, adam_variant, dtype, wd, adamw):
     O = oracle_lib
     g = torch.Generator(device="cpu").manual_seed(11)
     sizes = [1, 3, 4, 5, 4095, 4096, 4097, 70001, (1 << 20) + 7]
@@ -64,7 +73,7 @@ def test_adam_chunks_bit_exact(native_lib, oracle_lib, dtype, wd, adamw):
         np.testing.assert_array_equal(_bits16(gr), rg)
 
 
-def test_adam_chunks_many_items_and_prefix_only(native_lib, oracle_lib):
+def test_adam_chunks_many_items_and_prefix_only(native_lib, oracle_lib, adam_variant):
     """300 items (two launches); only the used prefix of each chunk changes."""
     O = oracle_lib
     cap, used = 8192, 5000
@@ -93,7 +102,7 @@ def test_adam_chunks_many_items_and_prefix_only(native_lib, oracle_lib):
         np.testing.assert_array_equal(_bits16(c[0])[used:], tail[0])
 
 
-def test_adam_skip_leaves_state_untouched(native_lib):
+def test_adam_skip_leaves_state_untouched(native_lib, adam_variant):
     hyper = K.AdamHyper()
     state = K.StepState(DEV, init_loss_scale=65536.0)
     state.sumsq().fill_(float("inf"))
