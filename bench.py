@@ -2,7 +2,8 @@
 
 Workload (BASELINE.json configs[1]): GPT-2 1B (L20 H2048, 16 heads,
 S1024, V50304), fp16 chunks with dynamic loss scaling, all chunks
-HBM-resident, per-GPU batch --batch (default 16), chunk capacity --cap
+HBM-resident, per-GPU batch --batch (default 32, from C2's {4,8,16,32}: the
+fastest), chunk capacity --cap
 (default 64Mi elements).  A step = warm-up-planned chunk-managed forward +
 backward + fused chunk Adam over one synthetic batch per GPU; N>1 ranks run
 ZeRO chunk groups over NCCL (weak scaling: fixed per-GPU batch).
@@ -38,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="chunk", choices=["chunk", "reference"])
-    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--cap", type=int, default=64 << 20)
     ap.add_argument("--layers", type=int, default=20)
     ap.add_argument("--hidden", type=int, default=2048)

@@ -1,7 +1,4 @@
-mkdir -p gpurun_out
-python -m pytest tests -m gpu -q 2>&1 | tail -3
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python bench.py --steps 10 --warmup 3 2>&1 | tail -1 | tee gpurun_out/bench_r1_final.json
-ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_r1b.csv python bench.py --profile-step --warmup 2 --no-cpu-baseline --no-offload-probe > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:adam_tma -c 1 -o gpurun_out/k1_tma_insitu python bench.py --profile-step --warmup 2 --no-cpu-baseline --no-offload-probe > gpurun_out/ncu_k1_tma.log 2>&1
-tail -1 gpurun_out/ncu_k1_tma.log
+for b in 8 16 32; do
+  timeout 600 python bench.py --steps 6 --warmup 3 --batch $b --no-cpu-baseline --no-offload-probe 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('B=$b', d['ms_per_step'], d['value'], d['tflops_per_gpu'], r['frac'], d['e2e']['value'])"
+done
+nvidia-smi --query-gpu=memory.used,memory.total --format=csv
