@@ -1,0 +1,92 @@
+"""Single-GPU measurements of the BASELINE configs reachable on one B200.
+
+* C2: 1B GPT, chunk-size sweep 32/64/128/256 Mi elements (B=32).
+* C3 model on one GPU: 4B GPT (L64 H2304), all chunks HBM-resident.
+* C4 mechanism on one GPU: 4B GPT with every optimizer triplet in pinned host
+  DRAM (os_placement=cpu): grads D2H, host fused Adam, params H2D per step.
+
+Each configuration runs in its own process (clean allocator); prints one
+JSON line per configuration.  Usage: python scripts/configs_sweep.py [which]
+"""
+
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+MI = 1 << 20
+CONFIGS = {
+    "1b_cap32": dict(layers=20, hidden=2048, heads=16, batch=32, cap=32 * MI, os="auto"),
+    "1b_cap64": dict(layers=20, hidden=2048, heads=16, batch=32, cap=64 * MI, os="auto"),
+    "1b_cap128": dict(layers=20, hidden=2048, heads=16, batch=32, cap=128 * MI, os="auto"),
+    "1b_cap256": dict(layers=20, hidden=2048, heads=16, batch=32, cap=256 * MI, os="auto"),
+    "4b_gpu": dict(layers=64, hidden=2304, heads=16, batch=8, cap=64 * MI, os="auto"),
+    "4b_os_cpu": dict(layers=64, hidden=2304, heads=16, batch=8, cap=64 * MI, os="cpu"),
+}
+
+
+def run_one(name: str) -> dict:
+    import torch
+    from paper_2108_05818_b200 import kernels as K
+    from paper_2108_05818_b200.config import PolicySpec
+    from paper_2108_05818_b200.model import build_gpt_schema
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CONFIGS[name]
+    schema = build_gpt_schema(layers=c["layers"], hidden_dim=c["hidden"], heads=c["heads"],
+                              seq_len=1024, vocab=50304, batch=c["batch"])
+    t_init = time.perf_counter()
+    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=c["cap"], os_placement=c["os"]),
+                      seed=0, hyper=K.AdamHyper(lr=1e-4), cuda_graph=True)
+    t_init = time.perf_counter() - t_init
+    gen = torch.Generator().manual_seed(3)
+    toks = [torch.randint(0, 50304, (c["batch"], 1025), generator=gen).cuda() for _ in range(2)]
+    warm = 4 if c["os"] == "cpu" else 7
+    for i in range(warm):
+        tr.step(toks[i % 2])
+    torch.cuda.synchronize()
+    steps = 3 if c["os"] == "cpu" else 6
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(steps):
+        loss = tr.step(toks[i % 2])
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    L, H, B, S, V = c["layers"], c["hidden"], c["batch"], 1024, 50304
+    flops = 72.0 * B * S * L * H * H * (1 + S / (6.0 * H) + V / (12.0 * L * H))
+    cs = tr.sim.chunk_set
+    rep = tr.reports[-1]
+    return {"config": name, "params_chunked": schema.chunked_param_count,
+            "capacity_elems": c["cap"], "positions": cs.positions,
+            "waste_elems": cs.waste_elems, "os_placement": c["os"],
+            "os_positions_on_gpu": len(tr.sim.engine.plan.os_positions_on_gpu),
+            "batch": B, "ms_per_step": round(ms, 2),
+            "tokens_per_s": round(B * S / (ms * 1e-3), 1),
+            "tflops": round(flops / (ms * 1e-3) / 1e12, 1),
+            "pcie_bytes_per_step": rep.pcie_bytes, "cuda_graph": tr._graph is not None,
+            "host_adam_s_per_step": round(tr.executor.stats.host_adam_seconds /
+                                          max(1, tr.iteration - 1), 3),
+            "peak_hbm_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
+            "init_s": round(t_init, 1), "final_loss": round(float(loss.item()), 4)}
+
+
+def main():
+    which = sys.argv[1:] or list(CONFIGS)
+    if len(which) == 1 and which[0] in CONFIGS and os.environ.get("CS_SWEEP_CHILD"):
+        print(json.dumps(run_one(which[0])), flush=True)
+        return
+    for name in which:
+        env = dict(os.environ, CS_SWEEP_CHILD="1")
+        res = subprocess.run([sys.executable, __file__, name], env=env, capture_output=True,
+                             text=True, timeout=1800)
+        line = [l for l in res.stdout.splitlines() if l.startswith("{")]
+        print(line[-1] if line else json.dumps({"config": name, "error": res.stderr[-500:]}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
