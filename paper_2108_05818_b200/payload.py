@@ -60,16 +60,19 @@ class ChunkComm:
         self.rank = dist.get_rank(group)
         self.calls: List[Tuple[str, int]] = []
 
-    def all_gather_slab(self, slab: torch.Tensor) -> None:
-        """In place: slot ``rank`` of ``slab`` is this rank's contribution."""
+    def all_gather_slab(self, slab: torch.Tensor, async_op: bool = False):
+        """In place: slot ``rank`` of ``slab`` is this rank's contribution.
+        With ``async_op`` returns the Work; ``work.wait()`` orders the
+        caller's current stream after it (no host wait on NCCL)."""
         cap = slab.numel() // self.world
         mine = slab[self.rank * cap:(self.rank + 1) * cap]
-        dist.all_gather_into_tensor(slab, mine, group=self.group)
         self.calls.append(("all_gather", slab.numel() * slab.element_size()))
+        return dist.all_gather_into_tensor(slab, mine, group=self.group, async_op=async_op)
 
-    def reduce_scatter_avg(self, out: torch.Tensor, slab: torch.Tensor) -> None:
-        dist.reduce_scatter_tensor(out, slab, op=dist.ReduceOp.AVG, group=self.group)
+    def reduce_scatter_avg(self, out: torch.Tensor, slab: torch.Tensor, async_op: bool = False):
         self.calls.append(("reduce_scatter", slab.numel() * slab.element_size()))
+        return dist.reduce_scatter_tensor(out, slab, op=dist.ReduceOp.AVG, group=self.group,
+                                          async_op=async_op)
 
     def all_reduce_sum(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
@@ -91,6 +94,8 @@ class ExecStats:
     prefetch_hits: int = 0
     prefetch_discarded: int = 0
     prefetch_discarded_bytes: int = 0
+    gather_prefetch_issued: int = 0
+    gather_prefetch_hits: int = 0
     host_adam_seconds: float = 0.0
     copy_events: List[Tuple[str, int, "torch.cuda.Event", "torch.cuda.Event"]] = field(
         default_factory=list)
@@ -121,6 +126,16 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._retained: Dict[Tuple[int, str], torch.Tensor] = {}
         self._awaiting_gather: Set[int] = set()
         self._group_slab: Dict[int, torch.Tensor] = {}
+        # collectives in flight: chunk id -> Work its payload depends on;
+        # Works (with the buffers they use) not yet waited for
+        self._coll_work: Dict[int, object] = {}
+        self._inflight: List[Tuple[object, Tuple[torch.Tensor, ...]]] = []
+        self._gather_log: List[Tuple[int, int]] = []        # (event, group) this iteration
+        self._gather_sched: Dict[int, List[int]] = {}       # event -> groups (last iteration)
+        self._gather_prefetched: Dict[int, Tuple[torch.Tensor, object]] = {}
+        self._cur_event = -1
+        self.overlap_collectives = True
+        self.gather_depth = 0
         self._pending: List[Tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor, int]] = []
         self._pending_ids: Set[int] = set()
         self._prefetched: Dict[int, Tuple[torch.Tensor, "torch.cuda.Event"]] = {}
@@ -195,7 +210,21 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     # -- stream ordering ------------------------------------------------------------
 
+    def _wait_collective(self, cid: int) -> None:
+        work = self._coll_work.pop(cid, None)
+        if work is not None:
+            work.wait()  # the current stream waits for the collective
+
+    def wait_collectives(self) -> None:
+        """Order the current stream after every collective still in flight."""
+        for work, _ in self._inflight:
+            work.wait()
+        self._inflight.clear()
+        self._coll_work.clear()
+
     def wait_ready(self, chunk: Chunk, device: str) -> None:
+        if device == GPU:
+            self._wait_collective(chunk.chunk_id)
         ev = self.ready.pop((chunk.chunk_id, device), None)
         if ev is None:
             return
@@ -221,6 +250,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             d, done = hit
             self.stats.prefetch_hits += 1
         else:
+            if src == GPU:  # a reduce-scatter may still be writing the payload
+                self._wait_collective(chunk.chunk_id)
             s = self.payload[src][chunk.chunk_id]
             d = self._retained.pop((chunk.chunk_id, dst), None)
             if d is None:
@@ -280,6 +311,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._prefetch_sched = sched
 
     def before_event(self, ev, iteration: int) -> None:
+        self._cur_event = ev.index
+        if self.comm is not None and self.comm.world > 1:
+            self._prefetch_gathers(ev)
         if not self.prefetch_depth or not self._prefetch_sched:
             return
         cs = self.chunk_set
@@ -350,9 +384,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         cap = self.chunk_set.capacity_elems
         return slab[k * cap:(k + 1) * cap]
 
-    def all_gather(self, group: CommGroup, kind: str) -> None:
-        if self.comm is None:
-            raise RuntimeError("data-parallel gather without a communicator")
+    def _issue_gather(self, group: CommGroup):
+        """Fill this rank's slot of a fresh p×cap slab and all-gather it
+        (async when overlapping: the compute stream waits only at use)."""
         cap, p = self.chunk_set.capacity_elems, self.partition.nproc
         slab = torch.empty(p * cap, dtype=self.dtype, device=self.device)
         mine = self._group_slot(slab, self.rank)
@@ -367,7 +401,20 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             else:  # local payload lives on the host: stage it into our slot
                 self.wait_ready(local, CPU)
                 mine.copy_(self.tensor(local, CPU), non_blocking=True)
-        self.comm.all_gather_slab(slab)
+        work = self.comm.all_gather_slab(slab, async_op=self.overlap_collectives)
+        if work is not None:
+            self._inflight.append((work, (slab,)))
+        return slab, work
+
+    def all_gather(self, group: CommGroup, kind: str) -> None:
+        if self.comm is None:
+            raise RuntimeError("data-parallel gather without a communicator")
+        hit = self._gather_prefetched.pop(group.group_id, None)
+        if hit is not None:  # issued ahead from the previous iteration's gather log
+            slab, work = hit
+            self.stats.gather_prefetch_hits += 1
+        else:
+            slab, work = self._issue_gather(group)
         for k, q in enumerate(group.member_positions):
             if q is None or k == self.rank:
                 continue
@@ -375,7 +422,10 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.payload[GPU][remote.chunk_id] = self._group_slot(slab, k)
             self.ready.pop((remote.chunk_id, GPU), None)
             self._awaiting_gather.discard(remote.chunk_id)
+            if work is not None:
+                self._coll_work[remote.chunk_id] = work
         self._group_slab[group.group_id] = slab
+        self._gather_log.append((self._cur_event, group.group_id))
         self.stats.gathers += 1
 
     def reduce_scatter(self, group: CommGroup) -> None:
@@ -385,7 +435,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         slab = self._group_slab.get(group.group_id)
         if slab is None:
             slab = torch.empty(p * cap, dtype=self.dtype, device=self.device)
-        out = None
+        out, out_cid = None, None
         for k, q in enumerate(group.member_positions):
             slot = self._group_slot(slab, k)
             if q is None:
@@ -393,17 +443,34 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     slot.zero_()
                 continue
             member = self.chunk_set.param_chunk(q)
+            self.wait_ready(member, GPU)  # gathered / fetched data has landed
             src = self.tensor(member, GPU)
             if k == self.rank:
-                out = src
+                out, out_cid = src, member.chunk_id
             if src.data_ptr() != slot.data_ptr():
-                self.wait_ready(member, GPU)
                 slot.copy_(src)
         if out is None:
             out = torch.empty(cap, dtype=self.dtype, device=self.device)  # phantom owner
-        self.comm.reduce_scatter_avg(out, slab)
+        work = self.comm.reduce_scatter_avg(out, slab, async_op=self.overlap_collectives)
+        if work is not None:  # overlaps the next groups' backward; waited at first use
+            self._inflight.append((work, (slab, out)))
+            if out_cid is not None:
+                self._coll_work[out_cid] = work
         self._group_slab[group.group_id] = slab
         self.stats.reduce_scatters += 1
+
+    def _prefetch_gathers(self, ev) -> None:
+        """Issue the gathers the previous iteration made during the next
+        ``gather_depth`` events.  The schedule comes from a ledger every rank
+        shares, so all ranks issue the same NCCL calls in the same order."""
+        if not self.gather_depth or not self._gather_sched:
+            return
+        for j in range(ev.index + 1, ev.index + 1 + self.gather_depth):
+            for gid in self._gather_sched.get(j, ()):
+                if gid in self._gather_prefetched:
+                    continue
+                self._gather_prefetched[gid] = self._issue_gather(self.partition.groups[gid])
+                self.stats.gather_prefetch_issued += 1
 
     # -- StepExecutor ---------------------------------------------------------------------------
 
@@ -425,6 +492,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._plan = plan
         for cid in list(self._prefetched):  # prefetches never cross the ADAM event
             self._discard_prefetch(cs.chunks[cid])
+        self._gather_prefetched.clear()     # (their Works are still in _inflight)
+        self.wait_collectives()             # reduce-scatters into local chunks landed
         self._host_state = None
         emb_grads = []
         for param, _, _, _ in self.embedding:
@@ -536,6 +605,10 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._pending_ids = set()
 
     def on_adam_end(self) -> None:
+        sched: Dict[int, List[int]] = {}
+        for ev_index, gid in self._gather_log:
+            sched.setdefault(ev_index, []).append(gid)
+        self._gather_sched, self._gather_log = sched, []
         self._flush_adam()
         self._retain_req.clear()
         self._retained.clear()

@@ -55,7 +55,8 @@ class ChunkTrainer:
                  non_model_fn: Optional[Callable[[int], int]] = None,
                  host_threads: int = 0, time_copies: bool = False,
                  cuda_graph: bool = False, fused_ops: bool = True,
-                 prefetch_depth: int = 2, non_model: str = "analytic"):
+                 prefetch_depth: int = 2, non_model: str = "analytic",
+                 gather_depth: int = 2):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -115,6 +116,7 @@ class ChunkTrainer:
         self.reports: List[IterationReport] = []
         self.cuda_graph = cuda_graph
         self.prefetch_depth = prefetch_depth
+        self.gather_depth = gather_depth
         self._graph = None
         self._side = None
         self.graph_kernels_per_step = 0
@@ -212,8 +214,9 @@ class ChunkTrainer:
             self.executor.end_of_warmup()
             if self.tracer is not None:
                 self.tracer.freeze()
-        else:  # the schedule is at its fixed point: prefetch next iteration's fetches
+        else:  # the schedule is at its fixed point: prefetch next iteration's moves
             self.executor.prefetch_depth = self.prefetch_depth
+            self.executor.gather_depth = self.gather_depth
             self.executor.set_prefetch_schedule(report.transfers)
         self.iteration += 1
         return loss.detach()
@@ -292,6 +295,12 @@ class ChunkTrainer:
             return float(self.step(self._static_tokens).item())
         tokens = tokens_host.to(self.device, non_blocking=True)
         return float(self.step(tokens).item())
+
+    def close(self) -> None:
+        """Drop the hook references that tie the model to the trainer, so the
+        payloads are freed deterministically rather than by the cycle GC."""
+        self.model.driver.on_start = self.model.driver.on_finish = None
+        self._graph = None
 
     # -- inspection -----------------------------------------------------------------------------
 

@@ -1,3 +1,1 @@
-mkdir -p gpurun_out
-timeout 2400 python scripts/configs_sweep.py 2>&1 | tee gpurun_out/configs_sweep_r1.jsonl
-free -g | head -2
+python -m pytest tests -m gpu -q 2>&1 | tail -3

@@ -86,6 +86,8 @@ class HostDoubleExecutor(ChunkPayloadExecutor):
                 view.reshape(-1).copy_(torch.from_numpy(g))
 
     def on_adam_begin(self, iteration, plan=None):
+        self._gather_prefetched.clear()
+        self.wait_collectives()  # as the product: reduce-scatters into local chunks landed
         self.os_state.sumsq = 1.0
         self.O.adam_prepare(self.os_state, LR, B1, B2)
 
@@ -137,6 +139,7 @@ def _worker(rank, world, port, outdir):
             rep = sim.engine.run_iteration(it, warmup=(it == 0),
                                            plan_builder=sim._plan_builder() if it == 0 else None)
             assert rep.feasible
+            ex.gather_depth = 2  # as the trainer: prefetch gathers from the previous log
         final = {}
         for pos in sim.local:
             chunk = sim.chunk_set.param_chunk(pos)
@@ -147,6 +150,7 @@ def _worker(rank, world, port, outdir):
                     torch.int16).clone()
         torch.save({"observed": ex.observed, "final": final,
                     "gathers": ex.stats.gathers, "reduce_scatters": ex.stats.reduce_scatters,
+                    "gather_prefetch_hits": ex.stats.gather_prefetch_hits,
                     "collectives": [(c.group_id, c.kind) for r in [rep] for c in r.collectives]},
                     os.path.join(outdir, "rank%d.pt" % rank))
     finally:
@@ -188,6 +192,7 @@ def test_zero_chunk_groups_over_gloo(world, oracle_lib):
     n_tensors = len(param_tensor_specs(schema))
     for r, res in enumerate(results):
         assert res["gathers"] > 0 and res["reduce_scatters"] > 0
+        assert res["gather_prefetch_hits"] > 0  # async gathers issued ahead were adopted
         checked = 0
         for it, phase, tid, bits in res["observed"]:
             np.testing.assert_array_equal(bits.numpy(), seen[it][tid],

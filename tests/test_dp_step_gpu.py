@@ -61,6 +61,7 @@ def _worker(rank, world, port, outdir, case):
                                     for x in r.collectives]} for r in tr.reports]
         st = tr.executor.stats
         torch.save({"losses": losses, "reports": reports, "gathers": st.gathers,
+                    "gather_prefetch_hits": st.gather_prefetch_hits,
                     "reduce_scatters": st.reduce_scatters, "host_adam": st.host_adam_items,
                     "copies": st.copies},
                    os.path.join(outdir, "rank%d.pt" % rank))
@@ -84,6 +85,7 @@ def test_multi_rank_zero_step_on_one_gpu(case, world):
             assert mine["collectives"] == theirs["collectives"], r
         n_coll = sum(len(x["collectives"]) for x in res[r]["reports"])
         assert res[r]["gathers"] + res[r]["reduce_scatters"] == n_coll > 0
+        assert res[r]["gather_prefetch_hits"] > 0
 
     # single rank on the concatenated batch
     from paper_2108_05818_b200.config import HardwareSpec, PolicySpec

@@ -185,6 +185,9 @@ def test_measured_warmup_tracer_drives_the_same_decisions():
     tests/test_decisions_golden.py) reproduces every ledger row."""
     from paper_2108_05818_b200.scenario import Simulator
     from paper_2108_05818_b200.trainer import ChunkTrainer
+    import gc
+    gc.collect()  # earlier tests' trainers must not be freed mid-measurement
+    torch.cuda.empty_cache()
     c = CASES["tiny_tight"]
     schema = build_gpt_schema(**c["schema"])
     probe = ChunkTrainer(schema, PolicySpec(**c["policy"]),
