@@ -194,6 +194,14 @@ int cs_xent_bwd(void* logits, const int64_t* targets, const float* lse_rows,
                 const float* dloss, float scale, int64_t rows, int64_t vocab, int dtype,
                 void* stream);
 
+/* ---- MLP GEMMs with the GELU fused into the cuBLASLt epilogue --------------
+ * mode 0 (forward):  out = gelu(x·Wᵀ), aux = x·Wᵀ      W [O,K], x [T,K] row-major
+ * mode 1 (backward): out = (x·W) ⊙ gelu'(aux)          W [K,O], x = dy [T,K], aux [T,O]
+ * gelu = tanh approximation.  workspace: caller-owned device buffer. */
+int cs_gemm_gelu(int mode, const void* w, const void* x, void* out, void* aux, int64_t T,
+                 int64_t O, int64_t K, int dtype, void* workspace, int64_t ws_bytes,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,7 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libchunkstar_b200.so")
 
 CUDA_SOURCES = ["adam.cu", "adam_tma.cu", "pack.cu", "xent.cu"]
-HOST_SOURCES = ["host_adam.cpp", "capi.cpp"]
+HOST_SOURCES = ["host_adam.cpp", "capi.cpp", "gemm_gelu.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 ORACLE_DIR = os.path.join(ROOT, "oracle")
@@ -68,14 +68,17 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
               "-Xcompiler", "-fPIC", *common, "-c", os.path.join(CSRC, src), "-o", obj],
              verbose)
         objs.append(obj)
+    cuda_home = os.path.dirname(os.path.dirname(os.path.realpath(_nvcc()))) \
+        if os.path.sep in _nvcc() else "/usr/local/cuda"
     for src in HOST_SOURCES:
         obj = os.path.join(BUILD, src + ".o")
         _run(["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off",
-              *common, "-c", os.path.join(CSRC, src), "-o", obj], verbose)
+              *common, "-I", os.path.join(cuda_home, "include"), "-c",
+              os.path.join(CSRC, src), "-o", obj], verbose)
         objs.append(obj)
     tmp = LIB + ".tmp"
     _run([_nvcc(), *ARCH, "-shared", "-cudart", "shared", "-o", tmp, *objs,
-          "-Xcompiler", "-fopenmp", "-lgomp"], verbose)
+          "-Xcompiler", "-fopenmp", "-lgomp", "-lcublasLt"], verbose)
     os.replace(tmp, LIB)
     return LIB
 

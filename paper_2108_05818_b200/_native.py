@@ -73,6 +73,10 @@ SIGNATURES = {
                                            ctypes.POINTER(CsStepState), ctypes.c_int]),
     "cs_grad_sumsq_host": (ctypes.c_int, [ctypes.POINTER(CsGradItem), ctypes.c_int, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_double), ctypes.c_int]),
+    "cs_gemm_gelu": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+                                    ctypes.c_int64, ctypes.c_void_p]),
     "cs_xent_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                    ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p]),

@@ -79,6 +79,55 @@ class _ChunkLinearResFn(torch.autograd.Function):
         return dx, None, dy, None
 
 
+class _LinearGeluFn(torch.autograd.Function):
+    """mlp_in half: u = x Wᵀ (differentiable) and g = gelu(u) (not) from ONE
+    GEMM with the GELU_AUX epilogue (cs_gemm_gelu mode 0)."""
+
+    @staticmethod
+    def forward(ctx, x: torch.Tensor, weight: nn.Parameter, grad_sink: Callable):
+        from . import kernels as K
+        ctx.set_materialize_grads(False)
+        ctx.weight, ctx.grad_sink = weight, grad_sink
+        ctx.save_for_backward(x)
+        u, g = K.gemm_gelu_fwd(x.reshape(-1, x.shape[-1]), weight)
+        ctx.mark_non_differentiable(g)
+        shp = x.shape[:-1] + (weight.shape[0],)
+        return u.view(shp), g.view(shp)
+
+    @staticmethod
+    def backward(ctx, du: torch.Tensor, _dg):
+        (x,) = ctx.saved_tensors
+        w = ctx.weight
+        dx = du.matmul(w)
+        ctx.grad_sink(w, du.reshape(-1, du.shape[-1]), x.reshape(-1, x.shape[-1]))
+        return dx, None, None
+
+
+class _GeluLinearResFn(torch.autograd.Function):
+    """mlp_out half: y = residual + gelu(u) Wᵀ, given g = gelu(u) from the
+    forward epilogue; backward's dX GEMM applies gelu'(u) in its DGELU
+    epilogue (cs_gemm_gelu mode 1) and hands du straight to mlp_in."""
+
+    @staticmethod
+    def forward(ctx, g: torch.Tensor, u: torch.Tensor, weight: nn.Parameter,
+                residual: torch.Tensor, grad_sink: Callable):
+        ctx.weight, ctx.grad_sink = weight, grad_sink
+        ctx.save_for_backward(g, u)
+        shp = residual.shape
+        out = torch.addmm(residual.reshape(-1, shp[-1]), g.reshape(-1, g.shape[-1]), weight.t())
+        return out.view(shp)
+
+    @staticmethod
+    def backward(ctx, dy: torch.Tensor):
+        from . import kernels as K
+        g, u = ctx.saved_tensors
+        w = ctx.weight
+        dy2 = dy.reshape(-1, dy.shape[-1]).contiguous()
+        du = K.gemm_dgelu(dy2, w, u.reshape(-1, u.shape[-1]))
+        ctx.grad_sink(w, dy2, g.reshape(-1, g.shape[-1]))
+        return None, du.view(u.shape), None, dy, None
+
+
 class _FusedXentFn(torch.autograd.Function):
     """Mean token cross entropy of fp16/bf16 logits via cs_xent_fwd/bwd; the
     gradient overwrites the (dead) logits buffer."""
@@ -110,6 +159,7 @@ def write_grad_into_slot(w: nn.Parameter, dy2: torch.Tensor, x2: torch.Tensor) -
 class _SlotEnter(torch.autograd.Function):
     @staticmethod
     def forward(ctx, driver, ev_fwd, ev_bwd, *xs):
+        ctx.set_materialize_grads(False)
         ctx.driver, ctx.ev_bwd = driver, ev_bwd
         driver.start(ev_fwd)
         return tuple(x.view_as(x) for x in xs) if len(xs) > 1 else xs[0].view_as(xs[0])
@@ -123,6 +173,7 @@ class _SlotEnter(torch.autograd.Function):
 class _SlotExit(torch.autograd.Function):
     @staticmethod
     def forward(ctx, driver, ev_fwd, ev_bwd, *ys):
+        ctx.set_materialize_grads(False)
         ctx.driver, ctx.ev_bwd = driver, ev_bwd
         driver.finish(ev_fwd)
         return tuple(y.view_as(y) for y in ys) if len(ys) > 1 else ys[0].view_as(ys[0])
@@ -263,9 +314,19 @@ class GPTBlock(nn.Module):
         (h,) = self._slot("attn_out", (o, h), lambda x, r: (self._lin_res(x, wo, r),))
         b = F.layer_norm(h, (H,))
         w1a, w1b = self.slots["mlp_in"]
+        w2a, w2b = self.slots["mlp_out"]
+        if self.fused:  # GELU in the GEMM epilogues (forward GELU_AUX, backward DGELU)
+            sink = self.grad_sink
+            u1, g1, u2, g2 = self._slot(
+                "mlp_in", (b,), lambda x: _LinearGeluFn.apply(x, w1a, sink)
+                + _LinearGeluFn.apply(x, w1b, sink))
+            (h,) = self._slot(
+                "mlp_out", (g1, u1, g2, u2, h),
+                lambda a1, v1, a2, v2, r: (_GeluLinearResFn.apply(
+                    a2, v2, w2b, _GeluLinearResFn.apply(a1, v1, w2a, r, sink), sink),))
+            return h
         u1, u2 = self._slot("mlp_in", (b,), lambda x: (self._lin(x, w1a), self._lin(x, w1b)))
         g1, g2 = F.gelu(u1, approximate="tanh"), F.gelu(u2, approximate="tanh")
-        w2a, w2b = self.slots["mlp_out"]
         (h,) = self._slot("mlp_out", (g1, g2, h),
                           lambda x1, x2, r: (self._lin_res(x2, w2b, self._lin_res(x1, w2a, r)),))
         return h

@@ -250,3 +250,49 @@ def xent_bwd_(logits: torch.Tensor, targets: torch.Tensor, lse: torch.Tensor,
                                  float(scale), rows, vocab, _code(logits.dtype),
                                  _stream(stream)), "cs_xent_bwd")
     return logits
+
+
+_WORKSPACE = {}
+
+
+def _lt_workspace(device: torch.device) -> torch.Tensor:
+    ws = _WORKSPACE.get(device)
+    if ws is None:
+        ws = _WORKSPACE[device] = torch.empty(32 << 20, dtype=torch.uint8, device=device)
+    return ws
+
+
+def gemm_gelu_fwd(x2d: torch.Tensor, w: torch.Tensor,
+                  stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+    """(u, g) = (x·Wᵀ, gelu_tanh(x·Wᵀ)) in one cuBLASLt GEMM (GELU_AUX epilogue)."""
+    _need_cuda(x2d, w)
+    T, K = x2d.shape
+    O = w.shape[0]
+    if w.shape[1] != K or not x2d.is_contiguous() or not w.is_contiguous():
+        raise ValueError("gemm_gelu_fwd: shapes/contiguity")
+    g = torch.empty(T, O, dtype=x2d.dtype, device=x2d.device)
+    u = torch.empty(T, O, dtype=x2d.dtype, device=x2d.device)
+    ws = _lt_workspace(x2d.device)
+    N.check(N.load().cs_gemm_gelu(0, ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(x2d.data_ptr()),
+                                  ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(u.data_ptr()),
+                                  T, O, K, _code(x2d.dtype), ctypes.c_void_p(ws.data_ptr()),
+                                  ws.numel(), _stream(stream)), "cs_gemm_gelu(fwd)")
+    return u, g
+
+
+def gemm_dgelu(dy2d: torch.Tensor, w: torch.Tensor, u: torch.Tensor,
+               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """du = (dy·W) ⊙ gelu_tanh'(u) in one cuBLASLt GEMM (DGELU epilogue); W [K,O]."""
+    _need_cuda(dy2d, w, u)
+    T, K = dy2d.shape
+    O = w.shape[1]
+    if w.shape[0] != K or tuple(u.shape) != (T, O) or not dy2d.is_contiguous() \
+            or not w.is_contiguous() or not u.is_contiguous():
+        raise ValueError("gemm_dgelu: shapes/contiguity")
+    du = torch.empty(T, O, dtype=dy2d.dtype, device=dy2d.device)
+    ws = _lt_workspace(dy2d.device)
+    N.check(N.load().cs_gemm_gelu(1, ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(dy2d.data_ptr()),
+                                  ctypes.c_void_p(du.data_ptr()), ctypes.c_void_p(u.data_ptr()),
+                                  T, O, K, _code(dy2d.dtype), ctypes.c_void_p(ws.data_ptr()),
+                                  ws.numel(), _stream(stream)), "cs_gemm_gelu(bwd)")
+    return du
