@@ -194,6 +194,16 @@ int cs_xent_bwd(void* logits, const int64_t* targets, const float* lse_rows,
                 const float* dloss, float scale, int64_t rows, int64_t vocab, int dtype,
                 void* stream);
 
+/* ---- non-affine LayerNorm (eps inside rsqrt), residual grad folded in -------
+ * fwd: y = (x - mean) * rstd per row of [rows, H]; saves mean / rstd (fp32).
+ * bwd: dx = rstd * (dy - mean(dy) - xhat * mean(dy * xhat)) + dres (dres nullable).
+ * H must be 256 x {1,2,4,8,9,12,16} (cs_layernorm_supported). */
+int cs_layernorm_supported(int H);
+int cs_layernorm_fwd(const void* x, void* y, float* mean, float* rstd, int64_t rows, int H,
+                     float eps, int dtype, void* stream);
+int cs_layernorm_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
+                     const void* dres, void* dx, int64_t rows, int H, int dtype, void* stream);
+
 /* ---- MLP GEMMs with the GELU fused into the cuBLASLt epilogue --------------
  * mode 0 (forward):  out = gelu(x·Wᵀ), aux = x·Wᵀ      W [O,K], x [T,K] row-major
  * mode 1 (backward): out = (x·W) ⊙ gelu'(aux)          W [K,O], x = dy [T,K], aux [T,O]

@@ -79,30 +79,6 @@ class _ChunkLinearResFn(torch.autograd.Function):
         return dx, None, dy, None
 
 
-class _LinearGeluFn(torch.autograd.Function):
-    """mlp_in half: u = x Wᵀ (differentiable) and g = gelu(u) (not) from ONE
-    GEMM with the GELU_AUX epilogue (cs_gemm_gelu mode 0)."""
-
-    @staticmethod
-    def forward(ctx, x: torch.Tensor, weight: nn.Parameter, grad_sink: Callable):
-        from . import kernels as K
-        ctx.set_materialize_grads(False)
-        ctx.weight, ctx.grad_sink = weight, grad_sink
-        ctx.save_for_backward(x)
-        u, g = K.gemm_gelu_fwd(x.reshape(-1, x.shape[-1]), weight)
-        ctx.mark_non_differentiable(g)
-        shp = x.shape[:-1] + (weight.shape[0],)
-        return u.view(shp), g.view(shp)
-
-    @staticmethod
-    def backward(ctx, du: torch.Tensor, _dg):
-        (x,) = ctx.saved_tensors
-        w = ctx.weight
-        dx = du.matmul(w)
-        ctx.grad_sink(w, du.reshape(-1, du.shape[-1]), x.reshape(-1, x.shape[-1]))
-        return dx, None, None
-
-
 class _GeluLinearResFn(torch.autograd.Function):
     """mlp_out half: y = residual + gelu(u) Wᵀ, given g = gelu(u) from the
     forward epilogue; backward's dX GEMM applies gelu'(u) in its DGELU
@@ -126,6 +102,101 @@ class _GeluLinearResFn(torch.autograd.Function):
         du = K.gemm_dgelu(dy2, w, u.reshape(-1, u.shape[-1]))
         ctx.grad_sink(w, dy2, g.reshape(-1, g.shape[-1]))
         return None, du.view(u.shape), None, dy, None
+
+
+class _LNResFn(torch.autograd.Function):
+    """(LN(h), h): the residual stream passes through the LayerNorm function so
+    that its backward gets both gradients and returns LN_bwd(dy) + d_residual
+    from one kernel (cs_layernorm_bwd) — no autograd accumulation pass."""
+
+    @staticmethod
+    def forward(ctx, h: torch.Tensor):
+        from . import kernels as K
+        h2 = h.reshape(-1, h.shape[-1])
+        y, mean, rstd = K.layernorm_fwd(h2)
+        ctx.save_for_backward(h2, mean, rstd)
+        return y.view_as(h), h.view_as(h)
+
+    @staticmethod
+    def backward(ctx, dy: torch.Tensor, dres: torch.Tensor):
+        from . import kernels as K
+        h2, mean, rstd = ctx.saved_tensors
+        H = h2.shape[-1]
+        dx = K.layernorm_bwd(dy.reshape(-1, H).contiguous(), h2, mean, rstd,
+                             None if dres is None else dres.reshape(-1, H).contiguous())
+        return dx.view_as(dy)
+
+
+class _LNFn(torch.autograd.Function):
+    """Plain non-affine LayerNorm on cs_layernorm_fwd/bwd (the final LN)."""
+
+    @staticmethod
+    def forward(ctx, h: torch.Tensor):
+        from . import kernels as K
+        h2 = h.reshape(-1, h.shape[-1])
+        y, mean, rstd = K.layernorm_fwd(h2)
+        ctx.save_for_backward(h2, mean, rstd)
+        return y.view_as(h)
+
+    @staticmethod
+    def backward(ctx, dy: torch.Tensor):
+        from . import kernels as K
+        h2, mean, rstd = ctx.saved_tensors
+        H = h2.shape[-1]
+        return K.layernorm_bwd(dy.reshape(-1, H).contiguous(), h2, mean, rstd).view_as(dy)
+
+
+class _QKVFn(torch.autograd.Function):
+    """q, k, v = x Wqᵀ, x Wkᵀ, x Wvᵀ; backward accumulates dX = dq Wq + dk Wk
+    + dv Wv in the GEMM epilogue (beta = 1) instead of two add passes, then
+    writes each dW over its chunk slot."""
+
+    @staticmethod
+    def forward(ctx, x, wq, wk, wv, grad_sink):
+        ctx.ws, ctx.grad_sink = (wq, wk, wv), grad_sink
+        ctx.save_for_backward(x)
+        return F.linear(x, wq), F.linear(x, wk), F.linear(x, wv)
+
+    @staticmethod
+    def backward(ctx, dq, dk, dv):
+        (x,) = ctx.saved_tensors
+        x2 = x.reshape(-1, x.shape[-1])
+        ds = [d.reshape(-1, d.shape[-1]) for d in (dq, dk, dv)]
+        dx = torch.mm(ds[0], ctx.ws[0])
+        dx.addmm_(ds[1], ctx.ws[1])
+        dx.addmm_(ds[2], ctx.ws[2])
+        for w, d in zip(ctx.ws, ds):
+            ctx.grad_sink(w, d, x2)
+        return dx.view_as(x), None, None, None, None
+
+
+class _MLPInFn(torch.autograd.Function):
+    """Both mlp_in halves with the GELU_AUX epilogue; backward accumulates
+    dX = du1 W1a + du2 W1b in the GEMM epilogue."""
+
+    @staticmethod
+    def forward(ctx, x, wa, wb, grad_sink):
+        from . import kernels as K
+        ctx.set_materialize_grads(False)
+        ctx.ws, ctx.grad_sink = (wa, wb), grad_sink
+        ctx.save_for_backward(x)
+        x2 = x.reshape(-1, x.shape[-1])
+        u1, g1 = K.gemm_gelu_fwd(x2, wa)
+        u2, g2 = K.gemm_gelu_fwd(x2, wb)
+        ctx.mark_non_differentiable(g1, g2)
+        shp = x.shape[:-1] + (wa.shape[0],)
+        return u1.view(shp), g1.view(shp), u2.view(shp), g2.view(shp)
+
+    @staticmethod
+    def backward(ctx, du1, _dg1, du2, _dg2):
+        (x,) = ctx.saved_tensors
+        x2 = x.reshape(-1, x.shape[-1])
+        d1, d2 = du1.reshape(-1, du1.shape[-1]), du2.reshape(-1, du2.shape[-1])
+        dx = torch.mm(d1, ctx.ws[0])
+        dx.addmm_(d2, ctx.ws[1])
+        ctx.grad_sink(ctx.ws[0], d1, x2)
+        ctx.grad_sink(ctx.ws[1], d2, x2)
+        return dx.view_as(x), None, None, None
 
 
 class _FusedXentFn(torch.autograd.Function):
@@ -270,6 +341,7 @@ class GPTBlock(nn.Module):
                  fused: bool = False):
         super().__init__()
         self.fused = fused
+        self.fused_ln = False  # set when the LN kernels support the width (attach time)
         H = schema.hidden_dim
         self.heads, self.layer, self.driver, self.grad_sink = schema.heads, layer, driver, grad_sink
         shapes = {"qkv": [(H, H)] * 3, "attn_out": [(H, H)], "mlp_in": [(2 * H, H)] * 2,
@@ -297,13 +369,23 @@ class GPTBlock(nn.Module):
         ys = fn(*xs)
         return _bracket(_SlotExit, self.driver, fwd, bwd, ys)
 
+    def _ln(self, h):
+        """(LN(h), residual h) — fused kernels when the width is supported."""
+        if self.fused and self.fused_ln:
+            return _LNResFn.apply(h)
+        return F.layer_norm(h, (h.shape[-1],)), h
+
     def forward(self, h: torch.Tensor) -> torch.Tensor:
         B, S, H = h.shape
         nh = self.heads
-        a = F.layer_norm(h, (H,))
+        a, h = self._ln(h)
         wq, wk, wv = self.slots["qkv"]
-        q, k, v = self._slot("qkv", (a,), lambda x: (self._lin(x, wq), self._lin(x, wk),
-                                                     self._lin(x, wv)))
+        if self.fused:
+            q, k, v = self._slot("qkv", (a,), lambda x: _QKVFn.apply(x, wq, wk, wv,
+                                                                      self.grad_sink))
+        else:
+            q, k, v = self._slot("qkv", (a,), lambda x: (self._lin(x, wq), self._lin(x, wk),
+                                                         self._lin(x, wv)))
 
         def heads(t):
             return t.view(B, S, nh, H // nh).transpose(1, 2)
@@ -312,14 +394,13 @@ class GPTBlock(nn.Module):
         o = o.transpose(1, 2).reshape(B, S, H)
         (wo,) = self.slots["attn_out"]
         (h,) = self._slot("attn_out", (o, h), lambda x, r: (self._lin_res(x, wo, r),))
-        b = F.layer_norm(h, (H,))
+        b, h = self._ln(h)
         w1a, w1b = self.slots["mlp_in"]
         w2a, w2b = self.slots["mlp_out"]
         if self.fused:  # GELU in the GEMM epilogues (forward GELU_AUX, backward DGELU)
             sink = self.grad_sink
             u1, g1, u2, g2 = self._slot(
-                "mlp_in", (b,), lambda x: _LinearGeluFn.apply(x, w1a, sink)
-                + _LinearGeluFn.apply(x, w1b, sink))
+                "mlp_in", (b,), lambda x: _MLPInFn.apply(x, w1a, w1b, sink))
             (h,) = self._slot(
                 "mlp_out", (g1, u1, g2, u2, h),
                 lambda a1, v1, a2, v2, r: (_GeluLinearResFn.apply(
@@ -386,7 +467,10 @@ class ReferenceShapedGPT(nn.Module):
         h = _EmbeddingMark.apply(self.driver, efwd, ebwd, h)
         for blk in self.blocks:
             h = _LayerCheckpoint.apply(blk, h) if self.checkpointing else blk(h)
-        h = F.layer_norm(h, (self.schema.hidden_dim,))
+        if self.fused and self.blocks and self.blocks[0].fused_ln:
+            h = _LNFn.apply(h)
+        else:
+            h = F.layer_norm(h, (self.schema.hidden_dim,))
         logits = F.linear(h, self.wte)
         if self.fused:  # sm_100a fused loss kernels (cs_xent_fwd/bwd)
             return fused_cross_entropy(logits.view(B * S, -1), targets.reshape(B * S))

@@ -296,3 +296,36 @@ def gemm_dgelu(dy2d: torch.Tensor, w: torch.Tensor, u: torch.Tensor,
                                   T, O, K, _code(dy2d.dtype), ctypes.c_void_p(ws.data_ptr()),
                                   ws.numel(), _stream(stream)), "cs_gemm_gelu(bwd)")
     return du
+
+
+def layernorm_supported(H: int) -> bool:
+    return bool(N.load().cs_layernorm_supported(int(H)))
+
+
+def layernorm_fwd(x2d: torch.Tensor, eps: float = 1e-5,
+                  stream: Optional[torch.cuda.Stream] = None):
+    """Non-affine LN over the last dim of a contiguous [rows, H] tensor."""
+    _need_cuda(x2d)
+    rows, H = x2d.shape
+    y = torch.empty_like(x2d)
+    mean = torch.empty(rows, dtype=torch.float32, device=x2d.device)
+    rstd = torch.empty(rows, dtype=torch.float32, device=x2d.device)
+    N.check(N.load().cs_layernorm_fwd(ctypes.c_void_p(x2d.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                                      ctypes.c_void_p(mean.data_ptr()),
+                                      ctypes.c_void_p(rstd.data_ptr()), rows, H, float(eps),
+                                      _code(x2d.dtype), _stream(stream)), "cs_layernorm_fwd")
+    return y, mean, rstd
+
+
+def layernorm_bwd(dy2d: torch.Tensor, x2d: torch.Tensor, mean: torch.Tensor, rstd: torch.Tensor,
+                  dres2d: Optional[torch.Tensor] = None,
+                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    rows, H = x2d.shape
+    dx = torch.empty_like(x2d)
+    N.check(N.load().cs_layernorm_bwd(ctypes.c_void_p(dy2d.data_ptr()), ctypes.c_void_p(x2d.data_ptr()),
+                                      ctypes.c_void_p(mean.data_ptr()),
+                                      ctypes.c_void_p(rstd.data_ptr()),
+                                      ctypes.c_void_p(dres2d.data_ptr() if dres2d is not None else 0),
+                                      ctypes.c_void_p(dx.data_ptr()), rows, H, _code(x2d.dtype),
+                                      _stream(stream)), "cs_layernorm_bwd")
+    return dx

@@ -99,6 +99,9 @@ class ChunkTrainer:
             self.model = ReferenceShapedGPT(schema, dtype=dtype, placeholders=True,
                                             fused=fused_ops)
         self.shapes = reference_tensor_shapes(schema)
+        if fused_ops and K.layernorm_supported(schema.hidden_dim):
+            for blk in self.model.blocks:
+                blk.fused_ln = True
         self.model.attach_events(self.sim.timeline)
         self._events = self.sim.timeline.events
         self.model.driver.on_start = self._on_start

@@ -237,12 +237,14 @@ def test_fused_gpt_matches_unfused_gpt(native_lib):
     dW within 4e-3 of its max-norm — a few fp16 ulps at that scale)."""
     from paper_2108_05818_b200.gpt import ReferenceShapedGPT
     from paper_2108_05818_b200.model import build_gpt_schema
-    schema = build_gpt_schema(layers=2, hidden_dim=128, heads=4, seq_len=64, vocab=1000,
+    schema = build_gpt_schema(layers=2, hidden_dim=256, heads=4, seq_len=64, vocab=1000,
                               batch=2)
     models = {}
     for fused in (False, True):
         torch.manual_seed(0)
         m = ReferenceShapedGPT(schema, dtype=torch.float16, fused=fused).to(DEV)
+        for blk in m.blocks:
+            blk.fused_ln = fused  # cs_layernorm kernels (H=256 supported)
         for p in m.parameters():
             torch.nn.init.normal_(p, std=0.02)
         models[fused] = m
@@ -285,3 +287,27 @@ def test_gemm_gelu_epilogues_vs_torch_fp32(native_lib, dtype):
     ref = uu.grad
     s2 = ref.abs().amax(dim=1, keepdim=True)
     assert ((du.float() - ref).abs() <= tol * s2 + 1e-3).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("H", [256, 2048, 2304])
+def test_layernorm_kernels_vs_torch_fp32(native_lib, dtype, H):
+    """cs_layernorm_fwd/bwd (non-affine, residual grad folded in) vs a plain
+    PyTorch fp32 reference: outputs and dx within 2 ulps of the 16-bit result."""
+    gen = torch.Generator(device=DEV).manual_seed(H)
+    rows = 777
+    x = (torch.randn(rows, H, device=DEV, generator=gen) * 3 + 1).to(dtype)
+    dy = torch.randn(rows, H, device=DEV, generator=gen).to(dtype)
+    dres = torch.randn(rows, H, device=DEV, generator=gen).to(dtype)
+    y, mean, rstd = K.layernorm_fwd(x)
+    xr = x.float().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (H,), eps=1e-5)
+    yr.backward(dy.float())
+    ref_dx = xr.grad + dres.float()
+    dx = K.layernorm_bwd(dy, x, mean, rstd, dres)
+    ulp = 2 ** -10 if dtype == torch.float16 else 2 ** -7
+    for got, ref in ((y, yr.detach()), (dx, ref_dx)):
+        err = (got.float() - ref).abs()
+        assert (err <= 2 * ulp * ref.abs() + 4 * ulp * ref.abs().amax(dim=1, keepdim=True) * 1e-2
+                + 1e-3).all(), float(err.max())
+    assert not K.layernorm_supported(128)
