@@ -209,6 +209,64 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
     return out
 
 
+NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md; 900 nominal)
+
+
+def collective_probe(dev, cap, dtype, world, iters=5, warmup=2):
+    """The chunk-group collectives of the step, timed alone: all-gather of a
+    p x cap group slab and reduce-scatter(avg) back to one cap chunk
+    (`parallel.py:196-264`), each issued synchronously on the current stream
+    and bracketed by CUDA events there; max over ranks.  busbw = (p-1)*cap*
+    elem_bytes / t against the measured 770 GB/s peer copy."""
+    import torch
+    import torch.distributed as dist
+    slab = torch.empty(world * cap, dtype=dtype, device=dev).normal_()
+    out = torch.empty(cap, dtype=dtype, device=dev)
+    rank = dist.get_rank()
+    mine = slab[rank * cap:(rank + 1) * cap]
+    res = {}
+    for name, fn in (("all_gather", lambda: dist.all_gather_into_tensor(slab, mine)),
+                     ("reduce_scatter_avg",
+                      lambda: dist.reduce_scatter_tensor(out, slab, op=dist.ReduceOp.AVG))):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / iters], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        busbw = (world - 1) * cap * slab.element_size() / (ms * 1e-3) / 1e9
+        res[name] = {"ms": round(ms, 4), "busbw_gbs": round(busbw, 1),
+                     "frac": round(busbw / NVLINK_PEAK_GBS, 4)}
+    res.update({"group_slab_bytes": world * cap * slab.element_size(), "p": world,
+                "peak_gbs": NVLINK_PEAK_GBS,
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                "timing": "CUDA events on the issuing stream, %d back-to-back calls, max over "
+                          "ranks" % iters})
+    del slab, out
+    return res
+
+
+def k1_traffic(elements):
+    """Per-launch DRAM traffic of K1 from the committed `ncu --set full`
+    capture of the same in-step launch (profiles/), scaled to this launch's
+    element count when it differs; None if no capture is committed."""
+    path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        per_elem = (d["dram_bytes_read"] + d["dram_bytes_write"]) / d["elements"]
+        return round(per_elem * elements, 0), d["source"]
+    except Exception:
+        return None, None
+
+
 def cpu_baseline(schema_kw, sample_batch, steps=1):
     from oracle.cpu_step import CpuChunkStep
     from paper_2108_05818_b200.model import build_gpt_schema
@@ -382,6 +440,7 @@ def main():
     k1_bytes = 28.0 * (sum(k1_elems) / len(k1_elems)) if k1_elems else 0.0
     k1_gbs = k1_bytes / (k1_avg_ms * 1e-3) / 1e9 if k1_ms else None
     st = trainer.step_state()
+    traffic, traffic_src = k1_traffic(int(k1_bytes // 28))
     out = {
         "metric": METRIC, "value": round(tokens_per_step / (ms * 1e-3), 1), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -403,7 +462,7 @@ def main():
                      "achieved": round(k1_gbs, 1) if k1_gbs else None, "peak": hbm_peak,
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": round(k1_gbs / hbm_peak, 4) if k1_gbs else None,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_source": traffic_src,
                      "algorithmic_bytes_per_launch": k1_bytes,
                      "elements_per_launch": int(k1_bytes // 28),
                      "avg_launch_ms": round(k1_avg_ms, 4),
@@ -419,6 +478,21 @@ def main():
         "clocks": clk,
         "final_loss": final_loss, "loss_scale": st.loss_scale, "adam_steps": int(st.step),
     }
+    if world > 1:
+        from paper_2108_05818_b200.parallel import CollectiveScheme, closed_form_volume
+        rep = trainer.reports[-1]
+        out["collectives_per_step"] = {
+            "ledger_bytes_per_rank": int(sum(c.bytes for c in rep.collectives)),
+            "count": len(rep.collectives),
+            "closed_form_bytes_per_rank": int(closed_form_volume(
+                world, trainer.sim.partition.padded_param_elems,
+                CollectiveScheme.CHUNK_COLLECTIVE))}
+        del trainer, ex
+        torch.cuda.empty_cache()
+        try:
+            out["collectives"] = collective_probe(dev, args.cap, dtype, world)
+        except Exception as e:  # reported, never fatal
+            out["collectives"] = {"error": repr(e)[:300]}
     if world == 1 and not args.no_offload_probe:
         del trainer, ex
         torch.cuda.empty_cache()
