@@ -183,6 +183,25 @@ int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
 int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtype, double* out,
                        int n_threads);
 
+/* ---- host embedding operator (CPU-placed embedding) ----------------------------
+ * PatrickStar's device-aware operator placement (PAPER §5): when the plan puts
+ * the embedding on the CPU (`profiler.py:70-74` embedding_compute_device), its
+ * fp16/bf16 weights stay in pinned host DRAM and only one activation block
+ * crosses per pass (`engine.py:202-213`: B*S*H fp16 H2D at FWD, its gradient
+ * D2H at BWD).  Host pointers; synchronous; AVX2/F16C + OpenMP.
+ * fwd: out[i,:] = round(float(wte[tok[i],:]) + float(wpe[i % seq_len,:])).
+ * bwd (grad overwrite, `engine.py:177-190`): gwte[v,:] = round(sum over tokens
+ * i with tok[i]==v, ascending i, of float(dout[i,:])), 0 for rows no token hits;
+ * gwpe[s,:] = round(sum over b ascending of float(dout[b*seq_len+s,:])).
+ * gwte / gwpe may be the weight buffers themselves.  hidden % 8 == 0; every
+ * token must lie in [0, vocab) (CS_EINVAL otherwise). */
+int cs_embed_fwd_host(const int64_t* tokens, int64_t n_tokens, int seq_len, const void* wte,
+                      const void* wpe, int64_t vocab, int hidden, void* out, int dtype,
+                      int n_threads);
+int cs_embed_bwd_host(const int64_t* tokens, int64_t n_tokens, int seq_len, const void* dout,
+                      int64_t vocab, int hidden, void* gwte, void* gwpe, int dtype,
+                      int n_threads);
+
 /* ---- fused LM-head cross entropy (the GPT step's loss) ----------------------
  * Forward: per-row loss = logsumexp(logits_row) - logits_row[target] and the
  * row's logsumexp, one pass over fp16/bf16 logits [rows, vocab].  Backward:

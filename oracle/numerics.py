@@ -103,3 +103,43 @@ def to_half_bits(x: np.ndarray) -> np.ndarray:
 
 def from_half_bits(h: np.ndarray) -> np.ndarray:
     return h.view(np.float16).astype(np.float32)
+
+
+# -- host embedding operator (CPU-placed embedding; cs_embed_*_host) --------------
+# Restates the semantics `include/chunkstar_b200.h` declares for the lookup the
+# reference places on the CPU (`profiler.py:70-74`, `engine.py:202-213`) in
+# plain numpy: fp32 arithmetic, one rounding per output, sums in ascending
+# token order.  Forward is pinned to torch's `F.embedding(tok, wte) + wpe[:S]`
+# (tests/test_host_embed.py); bits in / bits out (uint16).
+
+def _widen(bits: np.ndarray, dtype: int) -> np.ndarray:
+    if dtype == FP16:
+        return bits.view(np.float16).astype(np.float32)
+    return (bits.astype(np.uint32) << 16).view(np.float32)
+
+
+def _narrow(x: np.ndarray, dtype: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if dtype == FP16:
+        return x.astype(np.float16).view(np.uint16)
+    u = x.view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def embed_fwd(tokens: np.ndarray, wte: np.ndarray, wpe: np.ndarray, dtype: int) -> np.ndarray:
+    """tokens [B, S] int64; wte [V, H], wpe [>=S, H] uint16 bits -> [B, S, H] bits."""
+    B, S = tokens.shape
+    return _narrow(_widen(wte[tokens], dtype) + _widen(wpe[:S], dtype)[None], dtype)
+
+
+def embed_bwd(tokens: np.ndarray, dout: np.ndarray, V: int, dtype: int):
+    """dout [B, S, H] bits -> (gwte [V, H], gwpe [S, H]) bits; sequential fp32
+    sums in ascending flat token order (np.add.at is unbuffered, in order)."""
+    B, S = tokens.shape
+    H = dout.shape[-1]
+    d = _widen(dout.reshape(B * S, H), dtype)
+    gw = np.zeros((V, H), dtype=np.float32)
+    np.add.at(gw, tokens.reshape(-1), d)
+    gp = np.zeros((S, H), dtype=np.float32)
+    np.add.at(gp, np.tile(np.arange(S), B), d)
+    return _narrow(gw, dtype), _narrow(gp, dtype)

@@ -6,7 +6,7 @@
 // extra elementwise pass.  Here the LN function passes h through as the
 // residual and its backward produces dh = LN_bwd(dy) + d_residual in one pass.
 //
-// One warp per row, 128-bit loads, fp32 statistics (two-pass in registers:
+// Forward: one warp per row, 128-bit loads, fp32 statistics (two-pass in registers:
 // mean, then centred variance), eps inside the rsqrt like torch.
 
 #include <cuda_bf16.h>
@@ -91,53 +91,68 @@ ln_fwd_kernel(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
 }
 
 // dx = rstd * (dy - mean(dy) - xhat * mean(dy * xhat)) + dres
-template <int DT, int NV>
-__global__ void __launch_bounds__(kWarps * 32)
-ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
-              const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
-              const uint16_t* __restrict__ dres, uint16_t* __restrict__ dx, int64_t rows, int H) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (row >= rows) return;
+//
+// One row per CTA of H/8 threads: each thread owns one 128-bit vector of dy,
+// x and dres, all three loads issued before the reduction (the warp-per-row
+// form held 64 elements/lane in 150 registers = 8 warps/SM and exposed the
+// dres load after the reduction; this form runs ~40 registers, up to 8 rows
+// in flight per SM).  Block reduction: warp shuffles, then one smem pass.
+template <int DT>
+__global__ void __launch_bounds__(1024)
+ln_bwd_row_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                  const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                  const uint16_t* __restrict__ dres, uint16_t* __restrict__ dx, int H) {
+  __shared__ float red[2][32];
+  const int64_t row = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
   const float mean = mean_in[row], rstd = rstd_in[row];
-  const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * H);
-  const uint4* xr = reinterpret_cast<const uint4*>(x + row * H);
-  uint4 a[NV], b[NV];
+  const int64_t base = row * (int64_t)H / 8 + t;
+  const uint4 a = __ldcs(reinterpret_cast<const uint4*>(dy) + base);
+  const uint4 b = __ldcs(reinterpret_cast<const uint4*>(x) + base);
+  uint4 r = make_uint4(0u, 0u, 0u, 0u);
+  if (dres) r = __ldcs(reinterpret_cast<const uint4*>(dres) + base);
+  const uint32_t* ua = reinterpret_cast<const uint32_t*>(&a);
+  const uint32_t* ub = reinterpret_cast<const uint32_t*>(&b);
+  const uint32_t* ur = reinterpret_cast<const uint32_t*>(&r);
+  float xh[8], g[8];
   float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    a[i] = __ldcs(dyr + i * 32 + lane);
-    b[i] = __ldcs(xr + i * 32 + lane);
-    const uint32_t* ua = reinterpret_cast<const uint32_t*>(&a[i]);
-    const uint32_t* ub = reinterpret_cast<const uint32_t*>(&b[i]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float g0 = lo<DT>(ua[k]), g1 = hi<DT>(ua[k]);
-      s1 += g0 + g1;
-      s2 += g0 * ((lo<DT>(ub[k]) - mean) * rstd) + g1 * ((hi<DT>(ub[k]) - mean) * rstd);
+  for (int k = 0; k < 4; ++k) {
+    g[2 * k] = lo<DT>(ua[k]);
+    g[2 * k + 1] = hi<DT>(ua[k]);
+    xh[2 * k] = (lo<DT>(ub[k]) - mean) * rstd;
+    xh[2 * k + 1] = (hi<DT>(ub[k]) - mean) * rstd;
+    s1 += g[2 * k] + g[2 * k + 1];
+    s2 += g[2 * k] * xh[2 * k] + g[2 * k + 1] * xh[2 * k + 1];
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    red[0][warp] = s1;
+    red[1][warp] = s2;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float v1 = lane < nwarps ? red[0][lane] : 0.f;
+    float v2 = lane < nwarps ? red[1][lane] : 0.f;
+    v1 = warp_sum(v1);
+    v2 = warp_sum(v2);
+    if (lane == 0) {
+      red[0][0] = v1;
+      red[1][0] = v2;
     }
   }
-  const float m1 = warp_sum(s1) / H, m2 = warp_sum(s2) / H;
-  const uint4* rr = dres ? reinterpret_cast<const uint4*>(dres + row * H) : nullptr;
-  uint4* dxr = reinterpret_cast<uint4*>(dx + row * H);
+  __syncthreads();
+  const float m1 = red[0][0] / H, m2 = red[1][0] / H;
+  uint4 o;
+  uint32_t* ou = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    uint4 r = make_uint4(0u, 0u, 0u, 0u);
-    if (rr) r = __ldcs(rr + i * 32 + lane);
-    const uint32_t* ua = reinterpret_cast<const uint32_t*>(&a[i]);
-    const uint32_t* ub = reinterpret_cast<const uint32_t*>(&b[i]);
-    const uint32_t* ur = reinterpret_cast<const uint32_t*>(&r);
-    uint4 o;
-    uint32_t* ou = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float x0 = (lo<DT>(ub[k]) - mean) * rstd, x1 = (hi<DT>(ub[k]) - mean) * rstd;
-      const float d0 = rstd * (lo<DT>(ua[k]) - m1 - x0 * m2) + (rr ? lo<DT>(ur[k]) : 0.f);
-      const float d1 = rstd * (hi<DT>(ua[k]) - m1 - x1 * m2) + (rr ? hi<DT>(ur[k]) : 0.f);
-      ou[k] = (uint32_t)from_f<DT>(d0) | ((uint32_t)from_f<DT>(d1) << 16);
-    }
-    dxr[i * 32 + lane] = o;
+  for (int k = 0; k < 4; ++k) {
+    const float d0 = rstd * (g[2 * k] - m1 - xh[2 * k] * m2) + lo<DT>(ur[k]);
+    const float d1 = rstd * (g[2 * k + 1] - m1 - xh[2 * k + 1] * m2) + hi<DT>(ur[k]);
+    ou[k] = (uint32_t)from_f<DT>(d0) | ((uint32_t)from_f<DT>(d1) << 16);
   }
+  reinterpret_cast<uint4*>(dx)[base] = o;
 }
 
 template <int DT, int NV>
@@ -149,13 +164,12 @@ void launch_fwd(const void* x, void* y, float* mean, float* rstd, int64_t rows, 
                                                       rows, H, eps);
 }
 
-template <int DT, int NV>
+template <int DT>
 void launch_bwd(const void* dy, const void* x, const float* mean, const float* rstd,
                 const void* dres, void* dx, int64_t rows, int H, cudaStream_t s) {
-  const unsigned grid = (unsigned)((rows + kWarps - 1) / kWarps);
-  ln_bwd_kernel<DT, NV><<<grid, kWarps * 32, 0, s>>>(
+  ln_bwd_row_kernel<DT><<<(unsigned)rows, H / 8, 0, s>>>(
       static_cast<const uint16_t*>(dy), static_cast<const uint16_t*>(x), mean, rstd,
-      static_cast<const uint16_t*>(dres), static_cast<uint16_t*>(dx), rows, H);
+      static_cast<const uint16_t*>(dres), static_cast<uint16_t*>(dx), H);
 }
 
 // dispatch on H / 256 (elements per lane / 8) for the supported widths
@@ -170,21 +184,6 @@ bool dispatch_fwd(const void* x, void* y, float* m, float* r, int64_t rows, int 
     case 9: launch_fwd<DT, 9>(x, y, m, r, rows, H, eps, s); return true;
     case 12: launch_fwd<DT, 12>(x, y, m, r, rows, H, eps, s); return true;
     case 16: launch_fwd<DT, 16>(x, y, m, r, rows, H, eps, s); return true;
-    default: return false;
-  }
-}
-
-template <int DT>
-bool dispatch_bwd(const void* dy, const void* x, const float* m, const float* r,
-                  const void* dres, void* dx, int64_t rows, int H, cudaStream_t s) {
-  switch (H / 256) {
-    case 1: launch_bwd<DT, 1>(dy, x, m, r, dres, dx, rows, H, s); return true;
-    case 2: launch_bwd<DT, 2>(dy, x, m, r, dres, dx, rows, H, s); return true;
-    case 4: launch_bwd<DT, 4>(dy, x, m, r, dres, dx, rows, H, s); return true;
-    case 8: launch_bwd<DT, 8>(dy, x, m, r, dres, dx, rows, H, s); return true;
-    case 9: launch_bwd<DT, 9>(dy, x, m, r, dres, dx, rows, H, s); return true;
-    case 12: launch_bwd<DT, 12>(dy, x, m, r, dres, dx, rows, H, s); return true;
-    case 16: launch_bwd<DT, 16>(dy, x, m, r, dres, dx, rows, H, s); return true;
     default: return false;
   }
 }
@@ -228,8 +227,8 @@ extern "C" int cs_layernorm_bwd(const void* dy, const void* x, const float* mean
   }
   if (rows == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (dtype == CS_FP16) dispatch_bwd<CS_FP16>(dy, x, mean, rstd, dres, dx, rows, H, s);
-  else dispatch_bwd<CS_BF16>(dy, x, mean, rstd, dres, dx, rows, H, s);
+  if (dtype == CS_FP16) launch_bwd<CS_FP16>(dy, x, mean, rstd, dres, dx, rows, H, s);
+  else launch_bwd<CS_BF16>(dy, x, mean, rstd, dres, dx, rows, H, s);
   cs::note_launches(1);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

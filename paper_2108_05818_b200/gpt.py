@@ -418,15 +418,21 @@ class ReferenceShapedGPT(nn.Module):
 
     def __init__(self, schema: ModelSchema, dtype: torch.dtype = torch.float16,
                  grad_sink: Callable = write_grad_into_slot, placeholders: bool = False,
-                 fused: bool = False):
+                 fused: bool = False, untied_head: bool = False):
         """``placeholders``: parameters start as empty tensors; their ``.data``
-        is bound to chunk slots (or embedding buffers) by the executor."""
+        is bound to chunk slots (or embedding buffers) by the executor.
+        ``untied_head``: the LM head has its own [V, H] weight (used when the
+        embedding is CPU-placed, :mod:`.embedding`)."""
         super().__init__()
         self.schema = schema
         self.driver = EventDriver()
         V, S, H = schema.vocab, schema.seq_len, schema.hidden_dim
         self.wte = nn.Parameter(torch.empty(0 if placeholders else (V, H), dtype=dtype))
         self.wpe = nn.Parameter(torch.empty(0 if placeholders else (S, H), dtype=dtype))
+        self.lm_head = (nn.Parameter(torch.empty(0 if placeholders else (V, H), dtype=dtype))
+                        if untied_head else None)
+        #: a CPU-placed embedding operator (HostEmbedding); None = GPU lookup
+        self.host_embedding = None
         self.fused = fused
         self.checkpointing = False
         self.blocks = nn.ModuleList([GPTBlock(schema, l, self.driver, dtype, grad_sink,
@@ -463,7 +469,10 @@ class ReferenceShapedGPT(nn.Module):
         B, S = tokens.shape
         efwd, ebwd = self.embedding_events
         self.driver.start(efwd)
-        h = F.embedding(tokens, self.wte) + self.wpe[:S]
+        if self.host_embedding is not None:
+            h = self.host_embedding.forward(tokens)
+        else:
+            h = F.embedding(tokens, self.wte) + self.wpe[:S]
         h = _EmbeddingMark.apply(self.driver, efwd, ebwd, h)
         for blk in self.blocks:
             h = _LayerCheckpoint.apply(blk, h) if self.checkpointing else blk(h)
@@ -471,7 +480,7 @@ class ReferenceShapedGPT(nn.Module):
             h = _LNFn.apply(h)
         else:
             h = F.layer_norm(h, (self.schema.hidden_dim,))
-        logits = F.linear(h, self.wte)
+        logits = F.linear(h, self.wte if self.lm_head is None else self.lm_head)
         if self.fused:  # sm_100a fused loss kernels (cs_xent_fwd/bwd)
             return fused_cross_entropy(logits.view(B * S, -1), targets.reshape(B * S))
         return F.cross_entropy(logits.float().view(B * S, -1), targets.reshape(B * S))

@@ -77,6 +77,23 @@ class StepState:
     def sumsq(self) -> torch.Tensor:
         return self._f32("sumsq")
 
+    def snapshot(self):
+        """Queue an async copy of the state into pinned memory on the current
+        stream (after the kernels enqueued so far, not after later ones);
+        :meth:`from_snapshot` waits for exactly that copy."""
+        host = torch.empty(self.NBYTES, dtype=torch.uint8, pin_memory=True)
+        host.copy_(self.buf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return host, ev
+
+    @staticmethod
+    def from_snapshot(snap) -> N.CsStepState:
+        host, ev = snap
+        ev.synchronize()
+        raw = bytes(host.numpy().tobytes())
+        return N.CsStepState.from_buffer_copy(raw[:ctypes.sizeof(N.CsStepState)])
+
     def read(self) -> N.CsStepState:
         """Host copy (synchronises the buffer's stream)."""
         raw = bytes(self.buf.cpu().numpy().tobytes())
@@ -132,6 +149,41 @@ def grad_sumsq_host(grads: Sequence[Tuple[torch.Tensor, int]], n_threads: int = 
     N.check(N.load().cs_grad_sumsq_host(arr, len(grads), _code(grads[0][0].dtype),
                                         ctypes.byref(out), int(n_threads)), "cs_grad_sumsq_host")
     return out.value
+
+
+def _host_contig(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("host embedding kernels need contiguous host tensors")
+
+
+def embed_fwd_host(tokens: torch.Tensor, wte: torch.Tensor, wpe: torch.Tensor,
+                   out: torch.Tensor, n_threads: int = 0) -> torch.Tensor:
+    """CPU-placed embedding lookup (cs_embed_fwd_host): tokens [B, S] int64,
+    wte [V, H], wpe [>=S, H], out [B, S, H] (all host, fp16/bf16)."""
+    _host_contig(tokens, wte, wpe, out)
+    if tokens.dtype != torch.int64:
+        raise TypeError("tokens must be int64")
+    B, S = tokens.shape
+    V, H = wte.shape
+    N.check(N.load().cs_embed_fwd_host(tokens.data_ptr(), B * S, S, wte.data_ptr(),
+                                       wpe.data_ptr(), V, H, out.data_ptr(), _code(wte.dtype),
+                                       int(n_threads)), "cs_embed_fwd_host")
+    return out
+
+
+def embed_bwd_host(tokens: torch.Tensor, dout: torch.Tensor, gwte: torch.Tensor,
+                   gwpe: torch.Tensor, n_threads: int = 0) -> None:
+    """Gradient of the lookup written over gwte [V, H] / gwpe [S, H]
+    (cs_embed_bwd_host; deterministic fp32 sums, ascending token order)."""
+    _host_contig(tokens, dout, gwte, gwpe)
+    B, S = tokens.shape
+    V, H = gwte.shape
+    if gwpe.shape[0] != S:
+        raise ValueError("gwpe must have seq_len rows")
+    N.check(N.load().cs_embed_bwd_host(tokens.data_ptr(), B * S, S, dout.data_ptr(), V, H,
+                                       gwte.data_ptr(), gwpe.data_ptr(), _code(gwte.dtype),
+                                       int(n_threads)), "cs_embed_bwd_host")
 
 
 def sumsq_partials() -> int:

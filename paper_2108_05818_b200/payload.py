@@ -144,6 +144,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.prefetch_depth = 0
         self._plan = None
         self._host_state = None
+        self._state_snap = None
+        #: CPU-placed embedding operator (embedding.HostEmbedding) or None
+        self.host_embedding = None
         self._placeholder = torch.empty(0, dtype=dtype, device=self.device)
         self.chunk_set: Optional[ChunkSet] = None
         #: test hook: called as observer("pre"|"post", items) around each K1 launch
@@ -512,8 +515,19 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             else:
                 self.wait_ready(chunk, CPU)
                 host_items.append((self.tensor(chunk, CPU), n))
+        he = self.host_embedding
+        if he is not None:
+            if not he.grads_ready:
+                raise RuntimeError("host embedding has no gradient at ADAM")
+            if self.comm is not None and self.comm.world > 1:
+                for g16, _ in he.grad_items():  # average over ranks on the GPU
+                    d = g16.to(self.device, non_blocking=True)
+                    self.comm.all_reduce_avg(d)
+                    g16.copy_(d)
         if self.comm is None or self.comm.rank == 0:
             dev_items += emb_grads  # replicated after the all-reduce: count once
+            if he is not None:
+                host_items += he.grad_items()
         host = K.grad_sumsq_host(host_items, self.host_threads) if host_items else 0.0
         self.partials[-1:].fill_(host)
         K.grad_sumsq(dev_items, self.partials[:-1], dtype=self.dtype)
@@ -522,6 +536,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.comm.all_reduce_sum(self.state.sumsq())
         K.adam_prepare(self.state, self.hyper, max_grad_norm=self.max_grad_norm,
                        dynamic_scale=self.dynamic_loss_scale)
+        if not torch.cuda.is_current_stream_capturing():
+            # host-side Adam waits for these scalars only, not for K1
+            self._state_snap = self.state.snapshot()
         # host-placed positions: drain their gradients D2H now, in walk order,
         # so host Adam on position k overlaps the copy of position k+1 (the
         # accounting bills the same rows at each position's turn)
@@ -571,7 +588,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             return
         if self._host_state is None:
             self._flush_adam()  # device positions update while the host works
-            self._host_state = self.state.read()  # one sync per step, only with host positions
+            self._host_state = self._step_scalars_on_host()
         for c in (param,) + triplet:
             self.wait_ready(c, CPU)
         p16 = self.tensor(param, CPU)
@@ -604,12 +621,29 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._pending = []
         self._pending_ids = set()
 
+    def _step_scalars_on_host(self):
+        """Host copy of this step's scalars (waits for adam_prepare only)."""
+        if self._state_snap is None:
+            return self.state.read()
+        return K.StepState.from_snapshot(self._state_snap)
+
     def on_adam_end(self) -> None:
         sched: Dict[int, List[int]] = {}
         for ev_index, gid in self._gather_log:
             sched.setdefault(ev_index, []).append(gid)
         self._gather_sched, self._gather_log = sched, []
         self._flush_adam()
+        he = self.host_embedding
+        if he is not None:  # CPU-placed embedding: host Adam overlaps K1
+            if self._host_state is None:
+                self._host_state = self._step_scalars_on_host()
+            t0 = time.perf_counter()
+            K.adam_chunks_host(he.adam_items(), self.hyper, self._host_state,
+                               self.host_threads)
+            dt = time.perf_counter() - t0
+            self.stats.host_adam_seconds += dt
+            he.host_seconds += dt
+            he.grads_ready = False
         self._retain_req.clear()
         self._retained.clear()
         self._predrained.clear()

@@ -30,7 +30,8 @@ from .config import HardwareSpec, PolicySpec
 from .engine import IterationReport
 from .gpt import ReferenceShapedGPT, reference_tensor_shapes
 from .memory import OOMError
-from .model import ModelSchema
+from .model import CPU, GPU, ModelSchema
+from .embedding import HostEmbedding
 from .payload import ChunkComm, ChunkPayloadExecutor
 from .scenario import Simulator
 
@@ -56,7 +57,8 @@ class ChunkTrainer:
                  host_threads: int = 0, time_copies: bool = False,
                  cuda_graph: bool = False, fused_ops: bool = True,
                  prefetch_depth: int = 2, non_model: str = "analytic",
-                 gather_depth: int = 2):
+                 gather_depth: int = 2, embedding_placement: str = "plan",
+                 untied_head: Optional[bool] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -95,9 +97,28 @@ class ChunkTrainer:
                              payload_backend=ex, collective_backend=ex, executor=ex,
                              non_model_fn=non_model_fn)
         self.nproc, self.rank = nproc, rank
+        # where the embedding operator physically runs: the reference's plan
+        # (`profiler.py:70-74`, set on the engine by the Simulator) unless forced
+        if embedding_placement == "plan":
+            embedding_placement = self.sim.engine.embedding_device
+        if embedding_placement not in (CPU, GPU):
+            raise ValueError("embedding_placement must be 'plan', 'cpu' or 'gpu'")
+        self.embedding_placement = embedding_placement
+        host_emb = embedding_placement == CPU
+        if untied_head is None:
+            untied_head = host_emb
+        if host_emb and not untied_head:
+            raise ValueError("a CPU-placed embedding needs an untied LM head")
         with torch.device(self.device):
             self.model = ReferenceShapedGPT(schema, dtype=dtype, placeholders=True,
-                                            fused=fused_ops)
+                                            fused=fused_ops, untied_head=untied_head)
+        self.host_embedding = None
+        if host_emb:
+            self.host_embedding = HostEmbedding(schema.vocab, schema.seq_len,
+                                                schema.hidden_dim, dtype, self.device,
+                                                threads=host_threads)
+            self.model.host_embedding = self.host_embedding
+            ex.host_embedding = self.host_embedding
         self.shapes = reference_tensor_shapes(schema)
         if fused_ops and K.layernorm_supported(schema.hidden_dim):
             for blk in self.model.blocks:
@@ -106,9 +127,15 @@ class ChunkTrainer:
         self._events = self.sim.timeline.events
         self.model.driver.on_start = self._on_start
         self.model.driver.on_finish = self._on_finish
+        # non-chunked GPU parameters updated by K1: the embedding when it is
+        # GPU-placed, else the (untied) LM head
         emb = []
-        emb_shapes = [(schema.vocab, schema.hidden_dim), (schema.seq_len, schema.hidden_dim)]
-        for p, shape in zip(self.model.embedding_parameters(), emb_shapes):
+        V, H = schema.vocab, schema.hidden_dim
+        gpu_params = ([] if host_emb else
+                      list(zip(self.model.embedding_parameters(), [(V, H), (schema.seq_len, H)])))
+        if untied_head:
+            gpu_params.append((self.model.lm_head, (V, H)))
+        for p, shape in gpu_params:
             master = torch.empty(shape, dtype=torch.float32, device=self.device)
             emb.append((p, master, torch.zeros_like(master), torch.zeros_like(master)))
         ex.attach(self.sim.chunk_set, self.sim.partition, rank,
@@ -153,8 +180,22 @@ class ChunkTrainer:
             ex.seed_host_payload(chunk, host16)
             ex.init32[pos] = host32
         n_chunked = len(self.shapes)
+        # wte (seed n), wpe (n+1) and an untied head (n+2): the same values
+        # wherever the embedding is placed
+        if self.host_embedding is not None:
+            w = []
+            for k, shape in enumerate([(self.schema.vocab, self.schema.hidden_dim),
+                                       (self.schema.seq_len, self.schema.hidden_dim)]):
+                gen.manual_seed(seed * 1_000_003 + n_chunked + k)
+                w.append(torch.empty(shape, device=self.device).normal_(0.0, 0.02,
+                                                                        generator=gen))
+            self.host_embedding.load(*w)
+            del w
+            first = 2
+        else:
+            first = 0
         for k, (p, master, m, v) in enumerate(emb):
-            gen.manual_seed(seed * 1_000_003 + n_chunked + k)
+            gen.manual_seed(seed * 1_000_003 + n_chunked + first + k)
             master.normal_(0.0, 0.02, generator=gen)
             p.data = torch.empty(master.shape, dtype=self.dtype, device=self.device)
             K.cast_pack([(p.data.view(-1), 0, master.view(-1), master.numel())])
@@ -246,7 +287,7 @@ class ChunkTrainer:
             return False
         moves = [t for t in b.transfers if t.chunk_id != "embedding"]
         plan = self.sim.engine.plan
-        return (not moves and plan is not None
+        return (not moves and plan is not None and self.host_embedding is None
                 and len(plan.os_positions_on_gpu) == len(self.sim.local)
                 and self.executor.stats.host_adam_items == 0)
 
@@ -297,6 +338,8 @@ class ChunkTrainer:
             self._static_tokens.copy_(tokens_host, non_blocking=True)
             return float(self.step(self._static_tokens).item())
         tokens = tokens_host.to(self.device, non_blocking=True)
+        if self.host_embedding is not None:  # the host lookup reads these, no D2H
+            self.host_embedding.host_tokens = tokens_host[:, :-1]
         return float(self.step(tokens).item())
 
     def close(self) -> None:

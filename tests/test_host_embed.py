@@ -1,0 +1,83 @@
+"""Host embedding operator (CPU-placed embedding, PAPER §5 device-aware
+placement; `profiler.py:70-74`, `engine.py:202-213`) vs the numpy oracle:
+bit-exact.  Host product code, so it runs without a GPU.  The oracle's
+forward is pinned to torch's own `F.embedding(tok, wte) + wpe[:S]`."""
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2108_05818_b200 import kernels as K
+
+CODE = {torch.float16: 0, torch.bfloat16: 1}
+
+
+def _bits(t):
+    return t.view(torch.int16).numpy().view(np.uint16)
+
+
+def _case(dtype, B, S, V, H, seed, repeat_tokens=False):
+    g = torch.Generator().manual_seed(seed)
+    hi = 7 if repeat_tokens else V
+    tok = torch.randint(0, hi, (B, S), generator=g)
+    wte = (torch.randn(V, H, generator=g) * 0.02).to(dtype)
+    wpe = (torch.randn(S, H, generator=g) * 0.02).to(dtype)
+    dout = (torch.randn(B, S, H, generator=g) * 4.0).to(dtype)
+    return tok, wte, wpe, dout
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("B,S,V,H,rep", [(2, 16, 97, 64, False), (4, 128, 512, 256, True),
+                                         (3, 5, 11, 8, False), (1, 1, 1, 16, False)])
+def test_embed_fwd_bwd_bit_exact(native_lib, oracle_lib, dtype, B, S, V, H, rep):
+    O = oracle_lib
+    tok, wte, wpe, dout = _case(dtype, B, S, V, H, seed=B * 1000 + H, repeat_tokens=rep)
+    out = torch.empty(B, S, H, dtype=dtype)
+    K.embed_fwd_host(tok, wte, wpe, out, n_threads=4)
+    ref = O.embed_fwd(tok.numpy(), _bits(wte), _bits(wpe), CODE[dtype])
+    assert np.array_equal(_bits(out), ref)
+    gwte = torch.full((V, H), 7.0, dtype=dtype)   # overwritten, including unhit rows
+    gwpe = torch.full((S, H), 7.0, dtype=dtype)
+    K.embed_bwd_host(tok, dout, gwte, gwpe, n_threads=3)
+    rw, rp = O.embed_bwd(tok.numpy(), _bits(dout), V, CODE[dtype])
+    assert np.array_equal(_bits(gwte), rw)
+    assert np.array_equal(_bits(gwpe), rp)
+
+
+def test_oracle_forward_pinned_to_torch(oracle_lib):
+    tok, wte, wpe, _ = _case(torch.float16, 4, 32, 300, 64, seed=5)
+    ref = F.embedding(tok, wte) + wpe[:32]
+    got = oracle_lib.embed_fwd(tok.numpy(), _bits(wte), _bits(wpe), 0)
+    assert np.array_equal(_bits(ref.contiguous()), got)
+
+
+def test_oracle_backward_close_to_float64():
+    import oracle.numerics as O
+    tok, _, _, dout = _case(torch.float16, 4, 32, 50, 64, seed=6, repeat_tokens=True)
+    gw, gp = O.embed_bwd(tok.numpy(), _bits(dout), 50, 0)
+    d = dout.double().view(-1, 64)
+    ref = torch.zeros(50, 64, dtype=torch.float64).index_add_(0, tok.view(-1), d)
+    np.testing.assert_allclose(gw.view(np.float16).astype(np.float64), ref.numpy(),
+                               rtol=2e-3, atol=2e-3)
+    np.testing.assert_allclose(gp.view(np.float16).astype(np.float64),
+                               dout.double().sum(0).numpy(), rtol=2e-3, atol=2e-3)
+
+
+def test_weights_may_be_overwritten_in_place(native_lib):
+    """The trainer writes the gradient over the weight buffers themselves."""
+    tok, wte, wpe, dout = _case(torch.float16, 2, 8, 13, 16, seed=9)
+    a, b = torch.empty(13, 16, dtype=torch.float16), torch.empty(8, 16, dtype=torch.float16)
+    K.embed_bwd_host(tok, dout, a, b)
+    K.embed_bwd_host(tok, dout, wte, wpe)
+    assert torch.equal(a, wte) and torch.equal(b, wpe)
+
+
+def test_out_of_range_token_rejected(native_lib):
+    from paper_2108_05818_b200._native import NativeError
+    tok, wte, wpe, dout = _case(torch.float16, 1, 4, 10, 8, seed=1)
+    tok[0, 2] = 10
+    with pytest.raises(NativeError, match="out of"):
+        K.embed_fwd_host(tok, wte, wpe, torch.empty(1, 4, 8, dtype=torch.float16))
+    with pytest.raises(NativeError):
+        K.embed_bwd_host(tok, dout, wte, wpe)

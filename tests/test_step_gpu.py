@@ -68,13 +68,18 @@ def test_real_step_ledgers_match_reference(case):
         assert got["transfers"] == theirs["transfers"], (case, mine.iteration)
         assert got["collectives"] == theirs["collectives"]
         assert got["samples"] == theirs["samples"]
-    # the executor moved exactly the bytes the ledger bills (chunk rows; the
-    # embedding rows are accounting-only)
+    # the executor moved exactly the bytes the ledger bills: chunk rows, and
+    # (CPU-placed embedding, the plan for C1) the activation rows
     chunk_rows = [t for r in tr.reports for t in r.transfers if t.chunk_id != "embedding"]
     h2d = sum(t.bytes for t in chunk_rows if (t.src, t.dst) == ("cpu", "gpu"))
     d2h = sum(t.bytes for t in chunk_rows if (t.src, t.dst) == ("gpu", "cpu"))
     st = tr.executor.stats
     assert st.h2d_bytes - st.prefetch_discarded_bytes == h2d and st.d2h_bytes == d2h
+    assert tr.sim.engine.embedding_device == tr.embedding_placement == "cpu"
+    emb_rows = [t for r in tr.reports for t in r.transfers if t.chunk_id == "embedding"]
+    he = tr.host_embedding
+    assert he.h2d_bytes == sum(t.bytes for t in emb_rows if t.src == "cpu") > 0
+    assert he.d2h_bytes == sum(t.bytes for t in emb_rows if t.src == "gpu") > 0
 
 
 def test_adam_inside_real_step_matches_oracle():
@@ -86,7 +91,7 @@ def test_adam_inside_real_step_matches_oracle():
     tr.step_host(toks[1])
     tr.step_host(toks[2])
     step_check.disarm(tr)
-    assert rec["checked"] >= 2 * (tr.sim.chunk_set.positions + 2)
+    assert rec["checked"] >= 2 * (tr.sim.chunk_set.positions + len(tr.executor.embedding))
     assert rec["mismatch"] == []
 
 
@@ -129,7 +134,8 @@ def test_cuda_graph_replay_matches_eager_steps():
     with sdpa_kernel(SDPBackend.MATH):
         for graph in (False, True):
             tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
-                              dtype=torch.float16, seed=0, cuda_graph=graph)
+                              dtype=torch.float16, seed=0, cuda_graph=graph,
+                              embedding_placement="gpu")  # graphs need no host operator
             losses = [tr.step_host(t) for t in toks]
             params = [tr.local_chunk_payload(p).cpu().clone()
                       for p in range(tr.sim.chunk_set.positions)]
@@ -222,3 +228,55 @@ def test_measured_warmup_tracer_drives_the_same_decisions():
     assert not values
     for mine, ref in zip(tr.reports, run.reports):
         assert _ledger(mine) == _ledger(ref)
+
+
+def test_cpu_placed_embedding_trains_like_gpu_placed():
+    """Device-aware embedding placement (`profiler.py:70-74`): the CPU-placed
+    operator (host lookup, activation H2D, gradient D2H, host scatter-add and
+    host Adam; weights never in HBM) trains the same model as the GPU-placed
+    one.  First loss bit-identical (same lookup, same head); later steps
+    within fp16 tolerance (the GPU embedding backward sums in another order)."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_cap256Ki"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 5)
+    out = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for place in ("cpu", "gpu"):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0, embedding_placement=place,
+                              untied_head=True)
+            out[place] = ([tr.step_host(t) for t in toks], tr)
+    cpu, gpu = out["cpu"][1], out["gpu"][1]
+    assert cpu.host_embedding is not None and gpu.host_embedding is None
+    assert cpu.model.wte.numel() == 0            # no embedding weights in HBM
+    assert len(cpu.executor.embedding) == 1 and len(gpu.executor.embedding) == 3
+    assert out["cpu"][0][0] == out["gpu"][0][0]
+    np.testing.assert_allclose(out["cpu"][0], out["gpu"][0], rtol=2e-3)
+    he = cpu.host_embedding
+    w_gpu = gpu.model.wte.detach().float().cpu()
+    np.testing.assert_allclose(he.wte.float().numpy(), w_gpu.numpy(), atol=2e-3)
+    # every step moved B*S*H fp16 down and up, nothing else for the embedding
+    u = schema.batch * schema.seq_len * schema.hidden_dim * 2
+    assert he.h2d_bytes == he.d2h_bytes == u * len(toks)
+
+
+def test_cpu_embedding_with_device_tokens():
+    """step() with device-resident tokens (one small D2H of the token ids)
+    equals step_host() with host tokens."""
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_cap1Mi"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 3)
+    runs = []
+    for dev in (False, True):
+        tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                          dtype=torch.float16, seed=0)
+        assert tr.host_embedding is not None
+        if dev:
+            runs.append([float(tr.step(t.cuda()).item()) for t in toks])
+        else:
+            runs.append([tr.step_host(t) for t in toks])
+    assert runs[0][0] == runs[1][0]
+    np.testing.assert_allclose(runs[0], runs[1], rtol=1e-3)
