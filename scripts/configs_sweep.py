@@ -4,6 +4,12 @@
 * C3 model on one GPU: 4B GPT (L64 H2304), all chunks HBM-resident.
 * C4 mechanism on one GPU: 4B GPT with every optimizer triplet in pinned host
   DRAM (os_placement=cpu): grads D2H, host fused Adam, params H2D per step.
+* C4 model on ONE GPU: 12B GPT (L60 H4096) — with activation checkpointing
+  (plan keeps every optimizer triplet in HBM, a few fp16 chunks evicted), and
+  without (the warm-up plan splits the triplets between HBM and pinned host
+  DRAM: HBM + host RAM as one heterogeneous space).
+* Embedding operator placement at 1B B=16: the plan's CPU-placed embedding
+  against the same step with the embedding forced onto the GPU.
 
 Each configuration runs in its own process (clean allocator); prints one
 JSON line per configuration.  Usage: python scripts/configs_sweep.py [which]
@@ -26,6 +32,13 @@ CONFIGS = {
     "1b_cap256": dict(layers=20, hidden=2048, heads=16, batch=32, cap=256 * MI, os="auto"),
     "4b_gpu": dict(layers=64, hidden=2304, heads=16, batch=8, cap=64 * MI, os="auto"),
     "4b_os_cpu": dict(layers=64, hidden=2304, heads=16, batch=8, cap=64 * MI, os="cpu"),
+    "12b_ckpt": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI, os="auto",
+                     ckpt=True),
+    "12b_mixed": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI, os="auto"),
+    "1b_b16_emb_plan": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
+                            os="auto"),
+    "1b_b16_emb_gpu": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
+                           os="auto", emb="gpu", untied=True),
 }
 
 
@@ -39,16 +52,19 @@ def run_one(name: str) -> dict:
     schema = build_gpt_schema(layers=c["layers"], hidden_dim=c["hidden"], heads=c["heads"],
                               seq_len=1024, vocab=50304, batch=c["batch"])
     t_init = time.perf_counter()
-    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=c["cap"], os_placement=c["os"]),
-                      seed=0, hyper=K.AdamHyper(lr=1e-4), cuda_graph=True)
+    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=c["cap"], os_placement=c["os"],
+                                         checkpointing=c.get("ckpt", False)),
+                      seed=0, hyper=K.AdamHyper(lr=1e-4), cuda_graph=True,
+                      embedding_placement=c.get("emb", "plan"), untied_head=c.get("untied"))
     t_init = time.perf_counter() - t_init
     gen = torch.Generator().manual_seed(3)
     toks = [torch.randint(0, 50304, (c["batch"], 1025), generator=gen).cuda() for _ in range(2)]
-    warm = 4 if c["os"] == "cpu" else 7
+    slow = c["os"] == "cpu" or c["layers"] >= 60
+    warm = 4 if slow else 7
     for i in range(warm):
         tr.step(toks[i % 2])
     torch.cuda.synchronize()
-    steps = 3 if c["os"] == "cpu" else 6
+    steps = 3 if slow else 6
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for i in range(steps):
@@ -71,7 +87,14 @@ def run_one(name: str) -> dict:
             "host_adam_s_per_step": round(tr.executor.stats.host_adam_seconds /
                                           max(1, tr.iteration - 1), 3),
             "peak_hbm_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
-            "init_s": round(t_init, 1), "final_loss": round(float(loss.item()), 4)}
+            "init_s": round(t_init, 1), "final_loss": round(float(loss.item()), 4),
+            "checkpointing": bool(c.get("ckpt", False)),
+            "embedding_device": tr.embedding_placement,
+            "host_embedding_s_per_step": (round(tr.host_embedding.host_seconds /
+                                                max(1, tr.iteration), 4)
+                                          if tr.host_embedding is not None else 0.0),
+            "chunk_moves_gb_per_step": round(sum(t.bytes for t in rep.transfers
+                                                 if t.chunk_id != "embedding") / 1e9, 2)}
 
 
 def main():
