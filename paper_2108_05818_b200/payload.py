@@ -32,6 +32,7 @@ allocator (chunk-sized blocks are recycled step to step), host slabs from
 its pinned caching host allocator.
 """
 
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Set, Tuple
@@ -45,6 +46,7 @@ from .engine import StepExecutor
 from .memory import PayloadBackend
 from .model import CPU, GPU
 from .parallel import CollectiveBackend, CommGroup, DpPartition
+from .slabs import SlabPool
 
 
 class ChunkComm:
@@ -157,7 +159,15 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def _setup_device(self, init_loss_scale: float) -> None:
         self.compute = torch.cuda.current_stream(self.device)
-        self.copy_stream = torch.cuda.Stream(self.device)
+        # one copy stream per direction: PCIe is full duplex, so evictions
+        # (D2H) and fetches (H2D) proceed concurrently
+        self.copy_stream = torch.cuda.Stream(self.device)      # H2D
+        self.d2h_stream = (self.copy_stream if os.environ.get("CS_COPY_STREAMS") == "1"
+                           else torch.cuda.Stream(self.device))
+        streams = [self.compute, self.copy_stream]
+        if self.d2h_stream is not self.copy_stream:
+            streams.append(self.d2h_stream)
+        self.slabs = SlabPool(self.device, streams)
         self.state = K.StepState(self.device, init_loss_scale)
         self.partials = torch.zeros(K.sumsq_partials() + 1, device=self.device)
 
@@ -186,19 +196,23 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def _alloc(self, chunk: Chunk, device: str) -> torch.Tensor:
         if device == GPU:
-            return torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk),
-                               device=self.device)
+            return self.slabs.take(chunk.capacity_elems, self._elem_dtype(chunk), self.compute)
         return torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk), pin_memory=True)
 
     def _alloc_for_copy(self, chunk: Chunk) -> torch.Tensor:
         """HBM destination of an H2D copy, taken from the copy stream's pool so
         the copy need not wait for the compute stream; the compute stream is
         registered as a user (it consumes the payload after `wait_ready`)."""
-        with torch.cuda.stream(self.copy_stream):
-            d = torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk),
-                            device=self.device)
+        d = self.slabs.take(chunk.capacity_elems, self._elem_dtype(chunk), self.copy_stream)
         d.record_stream(self.compute)
         return d
+
+    def _release(self, cid: int, t: torch.Tensor) -> None:
+        """A GPU payload leaves the executor: back to the slab pool once the
+        work already enqueued on it (incl. a collective writing it) is done."""
+        if cid in self._coll_work:
+            self._wait_collective(cid)
+        self.slabs.give(t)
 
     def tensor(self, chunk: Chunk, device: str) -> torch.Tensor:
         return self.payload[device][chunk.chunk_id]
@@ -267,12 +281,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def _transfer(self, s: torch.Tensor, d: torch.Tensor, src: str, dst: str,
                   prior: Optional["torch.cuda.Event"]):
-        """cudaMemcpyAsync of a whole payload on the copy stream; returns the
-        completion event consumers wait on (`wait_ready`).  D2H waits for the
-        compute stream (the payload must be final); H2D does not (its source
-        is host data already final, its destination came from the copy
-        stream's pool)."""
-        cs = self.copy_stream
+        """cudaMemcpyAsync of a whole payload on the copy stream of its
+        direction; returns the completion event consumers wait on
+        (`wait_ready`).  D2H waits for the compute stream (the payload must be
+        final); H2D does not (its source is host data already final, its
+        destination came from the H2D stream's pool).  A move that depends on
+        an earlier one (a fetch of a chunk just evicted) waits on its event."""
+        cs = self.d2h_stream if src == GPU else self.copy_stream
         if src == GPU:
             cs.wait_stream(self.compute)
         if prior is not None:
@@ -337,6 +352,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     def _discard_prefetch(self, chunk: Chunk) -> None:
         hit = self._prefetched.pop(chunk.chunk_id, None)
         if hit is not None:
+            self.slabs.give(hit[0])
             self.stats.prefetch_discarded += 1
             self.stats.prefetch_discarded_bytes += hit[0].numel() * hit[0].element_size()
 
@@ -353,6 +369,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         key = (cid, device)
         if device == CPU:
             self._discard_prefetch(chunk)
+        if cid in self._pending_ids:
+            self._flush_adam()  # K1 must update this payload before it is recycled
         t = self.payload[device].pop(cid, None)
         self._awaiting_gather.discard(cid)
         ev = self.ready.pop(key, None)
@@ -362,6 +380,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 if ev is not None:
                     self.ready[key] = ev
                 self._retained[key] = t
+                t = None
+        if t is not None and device == GPU:
+            self._release(cid, t)
         if device == GPU and chunk.list_kind is ChunkKind.PARAM_FP16:
             for tmeta in chunk.tensors:
                 if self._bound.get(tmeta.tensor_id) == cid:
@@ -645,6 +666,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             he.host_seconds += dt
             he.grads_ready = False
         self._retain_req.clear()
+        for (cid, dev), t in self._retained.items():
+            if dev == GPU:
+                self._release(cid, t)
         self._retained.clear()
         self._predrained.clear()
 

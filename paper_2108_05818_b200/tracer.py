@@ -50,6 +50,7 @@ class MemoryTracer:
         tensors = list(ex.payload[GPU].values()) + list(ex._group_slab.values())
         tensors += [t for t, _ in ex._prefetched.values()]
         tensors += [t for (cid, dev), t in ex._retained.items() if dev == GPU]
+        tensors += ex.slabs.free_tensors()  # recycled chunk slabs are chunk memory
         for t in tensors:
             st = t.untyped_storage()
             seen[st.data_ptr()] = st.nbytes()

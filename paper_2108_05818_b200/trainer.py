@@ -20,6 +20,7 @@ records the access trace; the placement plan is computed at its ADAM event
 """
 
 import os
+import time
 from typing import Callable, List, Optional, Tuple
 
 import torch
@@ -150,6 +151,7 @@ class ChunkTrainer:
         self._graph = None
         self._side = None
         self.graph_kernels_per_step = 0
+        self.phase_seconds = {"fwd": 0.0, "bwd": 0.0, "adam": 0.0}
 
     # -- initialisation ---------------------------------------------------------------
 
@@ -244,14 +246,21 @@ class ChunkTrainer:
         eng.begin_iteration(self.iteration, warm,
                             self.sim._plan_builder() if warm else None, self.sim.local)
         self._check()
+        t0 = time.perf_counter()
         inp, tgt = tokens[:, :-1], tokens[:, 1:]
         loss = self.model(inp, tgt)
+        t1 = time.perf_counter()
         (loss * self.executor.state.loss_scale()).backward()
+        t2 = time.perf_counter()
         adam = self._events[-1]
         eng.start_event(adam)
         self._check()
         eng.finish_event(adam)
         self._check()
+        ph = self.phase_seconds  # host time per phase (enqueue + any blocking waits)
+        ph["fwd"] += t1 - t0
+        ph["bwd"] += t2 - t1
+        ph["adam"] += time.perf_counter() - t2
         report = eng.end_iteration()
         self.reports.append(report)
         if warm:

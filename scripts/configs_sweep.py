@@ -65,6 +65,9 @@ def run_one(name: str) -> dict:
         tr.step(toks[i % 2])
     torch.cuda.synchronize()
     steps = 3 if slow else 6
+    hs0 = torch.cuda.host_memory_stats()
+    retries0 = torch.cuda.memory_stats().get("num_alloc_retries", 0)
+    ph0 = dict(tr.phase_seconds)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for i in range(steps):
@@ -72,6 +75,11 @@ def run_one(name: str) -> dict:
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
+    hs1 = torch.cuda.host_memory_stats()
+    retries = torch.cuda.memory_stats().get("num_alloc_retries", 0) - retries0
+    host_phase_ms = {k: round((tr.phase_seconds[k] - ph0[k]) * 1e3 / steps, 1) for k in ph0}
+    pinned = {k: hs1[k] - hs0.get(k, 0) for k in hs1
+              if isinstance(hs1[k], (int, float)) and hs1[k] != hs0.get(k, 0)}
     L, H, B, S, V = c["layers"], c["hidden"], c["batch"], 1024, 50304
     flops = 72.0 * B * S * L * H * H * (1 + S / (6.0 * H) + V / (12.0 * L * H))
     cs = tr.sim.chunk_set
@@ -89,6 +97,10 @@ def run_one(name: str) -> dict:
             "peak_hbm_gb": round(torch.cuda.max_memory_allocated() / 1e9, 1),
             "init_s": round(t_init, 1), "final_loss": round(float(loss.item()), 4),
             "checkpointing": bool(c.get("ckpt", False)),
+            "host_phase_ms_per_step": host_phase_ms,
+            "cuda_alloc_retries_during_timing": retries,
+            "alloc_conf": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", ""), "pinned_alloc_during_timing": pinned,
+            "pinned_stats_end": {k: v for k, v in hs1.items() if "current" in k or "peak" in k},
             "embedding_device": tr.embedding_placement,
             "host_embedding_s_per_step": (round(tr.host_embedding.host_seconds /
                                                 max(1, tr.iteration), 4)

@@ -1,9 +1,10 @@
 """Host-side profile of eager chunk-managed steps (where the enqueue time goes).
 
-    python scripts/profile_host.py [batch] [steps]
+    python scripts/profile_host.py [batch] [steps] [sweep-config]
 
-Runs the 1B bench model eagerly (no CUDA graph) and prints cProfile's top
-functions by own time over `steps` steps after warm-up."""
+Runs the 1B bench model (or a scripts/configs_sweep.py configuration)
+eagerly (no CUDA graph) and prints cProfile's top functions by own time over
+`steps` steps after warm-up."""
 
 import cProfile
 import os
@@ -23,10 +24,20 @@ def main():
     from paper_2108_05818_b200.trainer import ChunkTrainer
     B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-    schema = build_gpt_schema(layers=20, hidden_dim=2048, heads=16, seq_len=1024, vocab=50304,
-                              batch=B)
-    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=64 << 20), seed=0,
-                      hyper=K.AdamHyper(lr=1e-4))
+    if len(sys.argv) > 3:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from configs_sweep import CONFIGS
+        c = CONFIGS[sys.argv[3]]
+        B = c["batch"]
+        schema = build_gpt_schema(layers=c["layers"], hidden_dim=c["hidden"], heads=c["heads"],
+                                  seq_len=1024, vocab=50304, batch=B)
+        pol = PolicySpec(capacity_elems=c["cap"], os_placement=c["os"],
+                         checkpointing=c.get("ckpt", False))
+    else:
+        schema = build_gpt_schema(layers=20, hidden_dim=2048, heads=16, seq_len=1024,
+                                  vocab=50304, batch=B)
+        pol = PolicySpec(capacity_elems=64 << 20)
+    tr = ChunkTrainer(schema, pol, seed=0, hyper=K.AdamHyper(lr=1e-4))
     tok = torch.randint(0, 50304, (B, 1025)).cuda()
     for _ in range(3):
         tr.step(tok)
@@ -41,7 +52,8 @@ def main():
     torch.cuda.synchronize()
     tot = (time.perf_counter() - t0) / steps
     print("host enqueue %.1f ms/step, wall %.1f ms/step" % (host * 1e3, tot * 1e3))
-    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+    pstats.Stats(pr).sort_stats("cumtime").print_stats(30)
 
 
 if __name__ == "__main__":

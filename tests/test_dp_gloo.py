@@ -54,6 +54,16 @@ def _fake_grad(numel: int, rank: int) -> np.ndarray:
     return (((rank + 1) + (e % 7)) * 2.0 ** -10).astype(np.float16)
 
 
+class _NoSlabs:
+    """Host double of the HBM slab pool: payloads are plain host tensors."""
+
+    def give(self, t):
+        return False
+
+    def free_tensors(self):
+        return []
+
+
 class HostDoubleExecutor(ChunkPayloadExecutor):
     """Device primitives on the host; everything else is the product code."""
 
@@ -61,6 +71,7 @@ class HostDoubleExecutor(ChunkPayloadExecutor):
         from oracle import numerics as O
         self.O = O
         self.compute = self.copy_stream = self.state = None
+        self.slabs = _NoSlabs()
         self.os_state = O.step_state(1.0)
         self.observed = []
 
