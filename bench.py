@@ -485,7 +485,7 @@ def main():
             "ledger_bytes_per_rank": int(sum(c.bytes for c in rep.collectives)),
             "count": len(rep.collectives),
             "closed_form_bytes_per_rank": int(closed_form_volume(
-                world, trainer.sim.partition.padded_param_elems,
+                world, trainer.sim.partition.padded_param_elems(args.cap),
                 CollectiveScheme.CHUNK_COLLECTIVE))}
         del trainer, ex
         torch.cuda.empty_cache()

@@ -369,8 +369,6 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         key = (cid, device)
         if device == CPU:
             self._discard_prefetch(chunk)
-        if cid in self._pending_ids:
-            self._flush_adam()  # K1 must update this payload before it is recycled
         t = self.payload[device].pop(cid, None)
         self._awaiting_gather.discard(cid)
         ev = self.ready.pop(key, None)
@@ -382,6 +380,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 self._retained[key] = t
                 t = None
         if t is not None and device == GPU:
+            if cid in self._pending_ids:
+                self._flush_adam()  # K1 must update this payload before it is recycled
             self._release(cid, t)
         if device == GPU and chunk.list_kind is ChunkKind.PARAM_FP16:
             for tmeta in chunk.tensors:

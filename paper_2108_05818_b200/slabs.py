@@ -28,6 +28,7 @@ Two rules keep HBM shared with the model's activations:
   only drops chunk bytes when something else (activations) needs them.
 """
 
+import os
 from typing import Dict, List, Sequence, Tuple
 
 import torch
@@ -39,6 +40,7 @@ class SlabPool:
         self.device = torch.device(device)
         self.streams = list(streams)      # streams[0] allocates (the compute stream)
         self.max_free = max_free
+        self.disabled = os.environ.get("CS_SLABS") == "0"  # A/B switch: plain allocator
         self._free: Dict[Tuple[torch.dtype, int], List[Tuple[torch.Tensor, list]]] = {}
         self._owned: Dict[int, Tuple[torch.dtype, int]] = {}
         self.allocs = 0      # slabs created (the pool's high-water mark)
@@ -47,9 +49,12 @@ class SlabPool:
 
     def take(self, numel: int, dtype: torch.dtype, stream: torch.cuda.Stream) -> torch.Tensor:
         """A slab of ``numel`` elements, safe to use on ``stream``."""
+        if torch.cuda.is_current_stream_capturing() or self.disabled:
+            with torch.cuda.stream(stream):  # (capture: the graph's private pool)
+                return torch.empty(numel, dtype=dtype, device=self.device)
         key = (dtype, int(numel))
         lst = self._free.get(key)
-        if lst and not torch.cuda.is_current_stream_capturing():
+        if lst:
             t, events = lst.pop()
             for ev in events:
                 stream.wait_event(ev)
@@ -63,9 +68,8 @@ class SlabPool:
             ev.record(home)
             stream.wait_event(ev)
             t.record_stream(stream)
-        if not torch.cuda.is_current_stream_capturing():
-            self._owned[t.data_ptr()] = key
-            self.allocs += 1
+        self._owned[t.data_ptr()] = key
+        self.allocs += 1
         return t
 
     def give(self, t: torch.Tensor) -> bool:

@@ -315,8 +315,11 @@ class ChunkTrainer:
         with torch.cuda.graph(graph, stream=self._side):
             self._static_loss = self._eager_step(self._static_tokens)
         self.graph_kernels_per_step = _native.launch_count() - n0
-        if len(ex.k1_events) > n_ev:  # K1's event-record nodes, re-recorded by every replay
-            self.graph_k1 = ex.k1_events.pop()
+        # event-record nodes of the graph reference these events: they live with it
+        self._graph_events = ex.k1_events[n_ev:]
+        del ex.k1_events[n_ev:]
+        if self._graph_events:  # K1's event-record nodes, re-recorded by every replay
+            self.graph_k1 = self._graph_events[-1]
         ex.record_k1 = record
         self._graph = graph
         self._captured_key = self._ledger_key(self.reports[-1])

@@ -280,3 +280,19 @@ def test_cpu_embedding_with_device_tokens():
             runs.append([tr.step_host(t) for t in toks])
     assert runs[0][0] == runs[1][0]
     np.testing.assert_allclose(runs[0], runs[1], rtol=1e-3)
+
+
+def test_one_k1_launch_per_all_resident_step():
+    """All GPU-placed positions (+ the non-chunked GPU parameters) are
+    updated by ONE K1 launch per step — dropping stale host copies at ADAM
+    (note_write) must not split the batch."""
+    tr, schema = _trainer("tiny_cap1Mi")
+    toks = _tokens(schema, 3)
+    tr.step_host(toks[0])
+    ex = tr.executor
+    ex.record_k1 = True
+    for t in toks[1:]:
+        n0 = len(ex.k1_events)
+        tr.step_host(t)
+        assert len(ex.k1_events) == n0 + 1
+    ex.record_k1 = False
