@@ -255,6 +255,26 @@ class _SlotExit(torch.autograd.Function):
         return (None, None, None) + grads
 
 
+class _DeviceEmbedding(torch.autograd.Function):
+    """GPU-placed embedding lookup on the sm_100a kernels (cs_embed_fwd/bwd):
+    the host operator's exact semantics (embedding.py), one backward kernel
+    instead of torch's sort + segmented-reduce + scatter pipeline."""
+
+    @staticmethod
+    def forward(ctx, tokens, wte, wpe):
+        from . import kernels as K
+        ctx.save_for_backward(tokens)
+        ctx.vocab, ctx.seq_rows = wte.shape[0], wpe.shape[0]
+        return K.embed_fwd(tokens, wte, wpe)
+
+    @staticmethod
+    def backward(ctx, grad):
+        from . import kernels as K
+        (tokens,) = ctx.saved_tensors
+        gwte, gwpe = K.embed_bwd(tokens, grad, ctx.vocab, ctx.seq_rows)
+        return None, gwte, gwpe
+
+
 class _EmbeddingMark(torch.autograd.Function):
     """embedding.fwd finishes at the lookup; embedding.bwd is the gradient
     arriving at the embedding output (after l0.qkv.bwd), start and finish."""
@@ -471,6 +491,8 @@ class ReferenceShapedGPT(nn.Module):
         self.driver.start(efwd)
         if self.host_embedding is not None:
             h = self.host_embedding.forward(tokens)
+        elif self.fused:
+            h = _DeviceEmbedding.apply(tokens, self.wte, self.wpe)
         else:
             h = F.embedding(tokens, self.wte) + self.wpe[:S]
         h = _EmbeddingMark.apply(self.driver, efwd, ebwd, h)

@@ -186,6 +186,45 @@ def embed_bwd_host(tokens: torch.Tensor, dout: torch.Tensor, gwte: torch.Tensor,
                                        int(n_threads)), "cs_embed_bwd_host")
 
 
+def embed_fwd(tokens: torch.Tensor, wte: torch.Tensor, wpe: torch.Tensor,
+              stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """GPU-placed embedding lookup (cs_embed_fwd): tokens [B, S] int64 ->
+    [B, S, H]; same bits as :func:`embed_fwd_host`."""
+    _need_cuda(tokens, wte, wpe)
+    tok = tokens.contiguous()
+    if tok.dtype != torch.int64:
+        raise TypeError("tokens must be int64")
+    B, S = tok.shape
+    H = wte.shape[1]
+    out = torch.empty(B, S, H, dtype=wte.dtype, device=wte.device)
+    N.check(N.load().cs_embed_fwd(tok.data_ptr(), B * S, S, wte.data_ptr(), wpe.data_ptr(), H,
+                                  out.data_ptr(), _code(wte.dtype), _stream(stream)),
+            "cs_embed_fwd")
+    return out
+
+
+def embed_bwd(tokens: torch.Tensor, dout: torch.Tensor, vocab: int, seq_rows: int,
+              stream: Optional[torch.cuda.Stream] = None):
+    """(gwte [V, H], gwpe [seq_rows, H]) for the lookup's output gradient
+    (cs_embed_bwd; the stable sort of the token ids is torch plumbing).
+    Rows of gwpe beyond the sequence length are zero."""
+    _need_cuda(tokens, dout)
+    tok = tokens.contiguous().view(-1)
+    B, S = tokens.shape
+    H = dout.shape[-1]
+    d = dout.contiguous()
+    srt, order = torch.sort(tok, stable=True)
+    bounds = torch.arange(vocab + 1, device=tok.device, dtype=torch.int64)
+    row_start = torch.searchsorted(srt, bounds)
+    gwte = torch.empty(vocab, H, dtype=dout.dtype, device=dout.device)
+    gwpe = (torch.empty(S, H, dtype=dout.dtype, device=dout.device) if seq_rows == S else
+            torch.zeros(seq_rows, H, dtype=dout.dtype, device=dout.device))
+    N.check(N.load().cs_embed_bwd(order.data_ptr(), row_start.data_ptr(), B * S, S, d.data_ptr(),
+                                  vocab, H, gwte.data_ptr(), gwpe.data_ptr(),
+                                  _code(dout.dtype), _stream(stream)), "cs_embed_bwd")
+    return gwte, gwpe
+
+
 def sumsq_partials() -> int:
     n = N.load().cs_sumsq_partials()
     if n <= 0:

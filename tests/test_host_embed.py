@@ -81,3 +81,26 @@ def test_out_of_range_token_rejected(native_lib):
         K.embed_fwd_host(tok, wte, wpe, torch.empty(1, 4, 8, dtype=torch.float16))
     with pytest.raises(NativeError):
         K.embed_bwd_host(tok, dout, wte, wpe)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA GPU")
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("B,S,V,H,rep", [(2, 16, 97, 64, False), (4, 128, 512, 256, True),
+                                         (3, 5, 11, 8, False), (8, 64, 50304, 2048, False)])
+def test_device_embedding_bit_identical_to_host_and_oracle(native_lib, oracle_lib, dtype, B, S,
+                                                           V, H, rep):
+    """cs_embed_fwd/bwd (GPU-placed operator) == cs_embed_*_host == oracle."""
+    O = oracle_lib
+    tok, wte, wpe, dout = _case(dtype, B, S, V, H, seed=B * 7 + H, repeat_tokens=rep)
+    wpe_big = torch.cat([wpe, (torch.randn(3, H) * 0.02).to(dtype)])  # wpe has spare rows
+    out = K.embed_fwd(tok.cuda(), wte.cuda(), wpe_big.cuda()).cpu()
+    assert np.array_equal(_bits(out), O.embed_fwd(tok.numpy(), _bits(wte), _bits(wpe),
+                                                  CODE[dtype]))
+    gw, gp = K.embed_bwd(tok.cuda(), dout.cuda(), V, S + 3)
+    rw, rp = O.embed_bwd(tok.numpy(), _bits(dout), V, CODE[dtype])
+    assert np.array_equal(_bits(gw.cpu()), rw)
+    assert np.array_equal(_bits(gp[:S].cpu()), rp) and not bool(gp[S:].any())
+    hw, hp = torch.empty(V, H, dtype=dtype), torch.empty(S, H, dtype=dtype)
+    K.embed_bwd_host(tok, dout, hw, hp)
+    assert torch.equal(hw.view(torch.int16), gw.cpu().view(torch.int16))
