@@ -176,6 +176,7 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
     a.record()
     for i in range(steps):
         tr.step(toks[i % 2])
+    tr.finish_host_work()  # the last step's async host Adam is part of the step
     b_.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b_) / steps
@@ -203,7 +204,10 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
            "host_adam_gelem_per_s": round(
                sum(tr.sim.chunk_set.param_chunk(p).used_elems for p in tr.sim.local)
                / max((st.host_adam_seconds - host0) / steps, 1e-9) / 1e9, 3),
-           "prefetch_hits": st.prefetch_hits, "peak_source": "pinned cudaMemcpyAsync 1 GiB"}
+           "prefetch_hits": st.prefetch_hits, "prefetch_issued": st.prefetch_issued,
+           "prefetch_discarded": st.prefetch_discarded,
+           "async_host_adam": tr.executor.async_host_adam,
+           "peak_source": "pinned cudaMemcpyAsync 1 GiB"}
     del tr
     torch.cuda.empty_cache()
     return out

@@ -33,7 +33,9 @@ its pinned caching host allocator.
 """
 
 import os
+import threading
 import time
+from concurrent.futures import Future, ThreadPoolExecutor
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Set, Tuple
 
@@ -81,6 +83,20 @@ class ChunkComm:
 
     def all_reduce_avg(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.AVG, group=self.group)
+
+
+class _HostAdamJob:
+    """One CPU-placed position's host Adam, run by the executor's worker
+    thread; the param chunk's ``adam_copy`` H2D (`engine.py:265-267`) is
+    issued by whichever thread comes second: the worker right after the
+    update, or the main thread if the update already finished."""
+
+    def __init__(self, cids):
+        self.cids = tuple(cids)
+        self.lock = threading.Lock()
+        self.adam_done = False
+        self.h2d = None            # deferred (chunk, src tensor, dst tensor, prior event)
+        self.future: Optional[Future] = None
 
 
 @dataclass
@@ -147,6 +163,15 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._plan = None
         self._host_state = None
         self._state_snap = None
+        #: run host Adam of CPU-placed positions on a worker thread, overlapping
+        #: the main thread's enqueue of the rest of the step and the next one.
+        #: Opt-in: bit-identical, but at 1B with every triplet on the host it
+        #: measured within noise of the synchronous walk (365-385 vs 368-370
+        #: ms/step) — the host Adam slows down by as much as it overlaps.
+        self.async_host_adam = os.environ.get("CS_ASYNC_HOST_ADAM", "0") == "1"
+        self._worker: Optional[ThreadPoolExecutor] = None
+        self._jobs: Dict[int, _HostAdamJob] = {}   # chunk id -> unfinished job
+        self._stats_lock = threading.Lock()
         #: CPU-placed embedding operator (embedding.HostEmbedding) or None
         self.host_embedding = None
         self._placeholder = torch.empty(0, dtype=dtype, device=self.device)
@@ -215,6 +240,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.slabs.give(t)
 
     def tensor(self, chunk: Chunk, device: str) -> torch.Tensor:
+        self._join(chunk.chunk_id)
         return self.payload[device][chunk.chunk_id]
 
     def has(self, chunk: Chunk, device: str) -> bool:
@@ -239,7 +265,23 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._inflight.clear()
         self._coll_work.clear()
 
+    def _join(self, cid: int) -> None:
+        """Block until the host Adam job touching chunk ``cid`` (and its
+        deferred H2D issue) is done."""
+        job = self._jobs.get(cid)
+        if job is None:
+            return
+        job.future.result()
+        for c in job.cids:
+            if self._jobs.get(c) is job:
+                del self._jobs[c]
+
+    def join_host_work(self) -> None:
+        for cid in list(self._jobs):
+            self._join(cid)
+
     def wait_ready(self, chunk: Chunk, device: str) -> None:
+        self._join(chunk.chunk_id)
         if device == GPU:
             self._wait_collective(chunk.chunk_id)
         ev = self.ready.pop((chunk.chunk_id, device), None)
@@ -253,6 +295,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     # -- PayloadBackend ------------------------------------------------------------------
 
     def copy(self, chunk: Chunk, src: str, dst: str, moment: int, reason: str) -> None:
+        job = self._jobs.get(chunk.chunk_id)
+        if job is not None and src == CPU and dst == GPU:
+            if self._defer_h2d(job, chunk):
+                return
+        self._join(chunk.chunk_id)
         if chunk.chunk_id in self._pending_ids:
             self._flush_adam()  # the move must carry post-update bytes
         if src == GPU and chunk.chunk_id in self._awaiting_gather:
@@ -279,6 +326,40 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.ready[(chunk.chunk_id, dst)] = done
         self.payload[dst][chunk.chunk_id] = d
 
+    def _defer_h2d(self, job: _HostAdamJob, chunk: Chunk) -> bool:
+        """The updated params of a position whose host Adam is still running
+        go H2D as soon as the update finishes (from the worker); False if it
+        already finished (the caller copies now)."""
+        cid = chunk.chunk_id
+        s = self.payload[CPU][cid]
+        d = self._alloc_for_copy(chunk)
+        prior = self.ready.pop((cid, CPU), None)
+        with job.lock:
+            if job.adam_done:
+                self._jobs.pop(cid, None)
+                done = self._transfer(s, d, CPU, GPU, prior)
+                if done is not None:
+                    self.ready[(cid, GPU)] = done
+                self.payload[GPU][cid] = d
+                return True
+            job.h2d = (cid, s, d, prior)
+        self.payload[GPU][cid] = d
+        return True
+
+    def _run_host_adam(self, job: _HostAdamJob, item, state) -> None:
+        t0 = time.perf_counter()
+        K.adam_chunks_host([item], self.hyper, state, self.host_threads)
+        with self._stats_lock:
+            self.stats.host_adam_seconds += time.perf_counter() - t0
+        with job.lock:
+            job.adam_done = True
+            h2d = job.h2d
+            if h2d is not None:
+                cid, s, d, prior = h2d
+                done = self._transfer(s, d, CPU, GPU, prior)
+                if done is not None:
+                    self.ready[(cid, GPU)] = done
+
     def _transfer(self, s: torch.Tensor, d: torch.Tensor, src: str, dst: str,
                   prior: Optional["torch.cuda.Event"]):
         """cudaMemcpyAsync of a whole payload on the copy stream of its
@@ -301,13 +382,15 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             done.record(cs)
         if src == GPU:
             s.record_stream(cs)
-            self.stats.d2h_bytes += s.numel() * s.element_size()
-        if dst == GPU:
-            self.stats.h2d_bytes += d.numel() * d.element_size()
-        if t0 is not None:
-            self.stats.copy_events.append(("%s>%s" % (src, dst), d.numel() * d.element_size(),
-                                           t0, done))
-        self.stats.copies += 1
+        with self._stats_lock:  # the host-Adam worker issues H2Ds too
+            if src == GPU:
+                self.stats.d2h_bytes += s.numel() * s.element_size()
+            if dst == GPU:
+                self.stats.h2d_bytes += d.numel() * d.element_size()
+            if t0 is not None:
+                self.stats.copy_events.append(("%s>%s" % (src, dst),
+                                               d.numel() * d.element_size(), t0, done))
+            self.stats.copies += 1
         return done
 
     # -- prefetch from the previous iteration's ledger (the warm-up trace) ---------
@@ -357,7 +440,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.stats.prefetch_discarded_bytes += hit[0].numel() * hit[0].element_size()
 
     def materialize(self, chunk: Chunk, device: str) -> None:
-        key = (chunk.chunk_id, device)
+        key = (chunk.chunk_id, device)  # (no data access: a running host job may go on)
         t = self._retained.pop(key, None)
         if t is None and device == GPU and self._is_remote_param(chunk):
             self._awaiting_gather.add(chunk.chunk_id)  # the group slab will back it
@@ -366,6 +449,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def drop(self, chunk: Chunk, device: str) -> None:
         cid = chunk.chunk_id
+        job = self._jobs.get(cid)
+        if job is not None:
+            # a host job reads/writes the CPU payloads and, once deferred, the
+            # H2D destination; a retained host payload keeps its job running
+            if (device == CPU and (cid, CPU) not in self._retain_req) or \
+                    (device == GPU and job.h2d is not None):
+                self._join(cid)
         key = (cid, device)
         if device == CPU:
             self._discard_prefetch(chunk)
@@ -512,6 +602,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def on_adam_begin(self, iteration: int, plan=None) -> None:
         """Global grad norm / found-inf and the device step scalars."""
+        self.join_host_work()  # the previous step's host updates are complete
         cs = self.chunk_set
         self._plan = plan
         for cid in list(self._prefetched):  # prefetches never cross the ADAM event
@@ -614,11 +705,19 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self.wait_ready(c, CPU)
         p16 = self.tensor(param, CPU)
         p32, m, v = (self.tensor(c, CPU) for c in triplet)
-        t0 = time.perf_counter()
-        K.adam_chunks_host([(p16, p32, m, v, n)], self.hyper, self._host_state,
-                           self.host_threads)
-        self.stats.host_adam_seconds += time.perf_counter() - t0
+        item = (p16, p32, m, v, n)
         self.stats.host_adam_items += 1
+        if not self.async_host_adam:
+            t0 = time.perf_counter()
+            K.adam_chunks_host([item], self.hyper, self._host_state, self.host_threads)
+            self.stats.host_adam_seconds += time.perf_counter() - t0
+            return
+        if self._worker is None:
+            self._worker = ThreadPoolExecutor(max_workers=1, thread_name_prefix="cs-host-adam")
+        job = _HostAdamJob(c.chunk_id for c in (param,) + triplet)
+        for cid in job.cids:
+            self._jobs[cid] = job
+        job.future = self._worker.submit(self._run_host_adam, job, item, self._host_state)
 
     def retain_param_payload(self, chunk: Chunk, device: str) -> None:
         self._retain_req.add((chunk.chunk_id, device))
@@ -662,7 +761,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             K.adam_chunks_host(he.adam_items(), self.hyper, self._host_state,
                                self.host_threads)
             dt = time.perf_counter() - t0
-            self.stats.host_adam_seconds += dt
+            with self._stats_lock:
+                self.stats.host_adam_seconds += dt
             he.host_seconds += dt
             he.grads_ready = False
         self._retain_req.clear()
@@ -674,5 +774,6 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def end_of_warmup(self) -> None:
         """The fp32 init copies read zero-copy by K6 can go once it has run."""
+        self.join_host_work()
         torch.cuda.synchronize(self.device)
         self._keepalive = []

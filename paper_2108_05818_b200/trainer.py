@@ -59,7 +59,8 @@ class ChunkTrainer:
                  cuda_graph: bool = False, fused_ops: bool = True,
                  prefetch_depth: int = 2, non_model: str = "analytic",
                  gather_depth: int = 2, embedding_placement: str = "plan",
-                 untied_head: Optional[bool] = None):
+                 untied_head: Optional[bool] = None,
+                 async_host_adam: Optional[bool] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -88,6 +89,8 @@ class ChunkTrainer:
             dynamic_loss_scale=dynamic_loss_scale, max_grad_norm=max_grad_norm, comm=comm,
             host_threads=host_threads, time_copies=time_copies)
         ex = self.executor
+        if async_host_adam is not None:
+            ex.async_host_adam = async_host_adam
         self.tracer = None
         if non_model == "measured" and non_model_fn is None:
             from .tracer import MemoryTracer
@@ -353,6 +356,18 @@ class ChunkTrainer:
         if self.host_embedding is not None:  # the host lookup reads these, no D2H
             self.host_embedding.host_tokens = tokens_host[:, :-1]
         return float(self.step(tokens).item())
+
+    def finish_host_work(self) -> None:
+        """Wait for the host-side work a step may leave running (the async
+        host Adam of CPU-placed positions and its deferred H2D issues); GPU
+        work is stream-ordered behind it.  Call before timing the end of a
+        run or inspecting host payloads directly.  The current stream then
+        also waits for the copy streams (the deferred H2Ds of those updates)."""
+        ex = self.executor
+        ex.join_host_work()
+        cur = torch.cuda.current_stream(self.device)
+        for s in {ex.copy_stream, ex.d2h_stream}:
+            cur.wait_stream(s)
 
     def close(self) -> None:
         """Drop the hook references that tie the model to the trainer, so the

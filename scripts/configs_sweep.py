@@ -72,6 +72,7 @@ def run_one(name: str) -> dict:
     a.record()
     for i in range(steps):
         loss = tr.step(toks[i % 2])
+    tr.finish_host_work()
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps

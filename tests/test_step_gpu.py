@@ -59,6 +59,7 @@ def test_real_step_ledgers_match_reference(case):
     tr, schema = _trainer(case)
     ref = CASES[case]["ranks"]["0"]
     losses = [tr.step_host(t) for t in _tokens(schema, CASES[case]["iterations"])]
+    tr.finish_host_work()  # the last step's host Adam / adam_copy H2D may still be in flight
     assert all(np.isfinite(losses))
     assert [list(r) for r in tr.sim.chunk_set.layout_rows()] == ref["layout"]
     plan = tr.sim.engine.plan
@@ -295,3 +296,33 @@ def test_one_k1_launch_per_all_resident_step():
         tr.step_host(t)
         assert len(ex.k1_events) == n0 + 1
     ex.record_k1 = False
+
+
+@pytest.mark.parametrize("case", ["tiny_tight", "tiny_os_cpu"])
+def test_async_host_adam_matches_synchronous(case):
+    """Host Adam of CPU-placed positions on the worker thread (overlapping
+    the rest of the step and the next forward, its adam_copy H2D issued by
+    the worker) gives the synchronous run's bits, ledgers and moved bytes."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES[case]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 4)
+    runs = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for async_adam in (False, True):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0, async_host_adam=async_adam)
+            losses = [tr.step_host(t) for t in toks]
+            tr.finish_host_work()
+            params = [tr.local_chunk_payload(p).cpu().clone()
+                      for p in range(tr.sim.chunk_set.positions)]
+            st = tr.executor.stats
+            runs[async_adam] = (losses, params, [_ledger(r)["transfers"] for r in tr.reports],
+                                (st.h2d_bytes - st.prefetch_discarded_bytes, st.d2h_bytes),
+                                st.host_adam_items)
+    assert runs[True][4] > 0
+    assert runs[True][0] == runs[False][0]
+    for a, b in zip(runs[True][1], runs[False][1]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    assert runs[True][2] == runs[False][2] and runs[True][3] == runs[False][3]
