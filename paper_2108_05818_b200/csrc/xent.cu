@@ -44,6 +44,30 @@ __device__ __forceinline__ void online(float x, float& m, float& s) {
   }
 }
 
+// eight values at once: one max, at most one rescale, eight exp-adds (no
+// per-element divergent branch)
+template <int DT>
+__device__ __forceinline__ void online8(const uint4& w, float& m, float& s) {
+  const uint32_t* u = reinterpret_cast<const uint32_t*>(&w);
+  float v[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[2 * k] = to_f<DT>(u[k] & 0xffff);
+    v[2 * k + 1] = to_f<DT>(u[k] >> 16);
+  }
+  float mx = v[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) mx = fmaxf(mx, v[k]);
+  if (mx > m) {
+    s *= exp2f((m - mx) * kLog2e);
+    m = mx;
+  }
+  if (m == -INFINITY) return;
+  const float mb = m * kLog2e;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += exp2f(fmaf(v[k], kLog2e, -mb));
+}
+
 __device__ __forceinline__ void merge(float& m, float& s, float m2, float s2) {
   const float mx = fmaxf(m, m2);
   if (mx == -INFINITY) return;
@@ -62,15 +86,14 @@ xent_fwd_kernel(const uint16_t* __restrict__ logits, const int64_t* __restrict__
   if (vec) {
     const uint4* xv = reinterpret_cast<const uint4*>(x);
     const int64_t nv = vocab / 8;
-    for (int64_t i = threadIdx.x; i < nv; i += kThreads) {
-      const uint4 w = __ldcs(xv + i);
-      const uint32_t* u = reinterpret_cast<const uint32_t*>(&w);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        online(to_f<DT>(u[k] & 0xffff), m, s);
-        online(to_f<DT>(u[k] >> 16), m, s);
-      }
+    int64_t i = threadIdx.x;
+    for (; i + kThreads < nv; i += 2 * kThreads) {  // two 128-bit loads in flight
+      const uint4 w0 = __ldcs(xv + i);
+      const uint4 w1 = __ldcs(xv + i + kThreads);
+      online8<DT>(w0, m, s);
+      online8<DT>(w1, m, s);
     }
+    if (i < nv) online8<DT>(__ldcs(xv + i), m, s);
   } else {
     for (int64_t i = threadIdx.x; i < vocab; i += kThreads) online(to_f<DT>(x[i]), m, s);
   }
