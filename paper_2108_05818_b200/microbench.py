@@ -2,8 +2,10 @@
 
 Algorithmic bytes per element: K1 Adam 28, K2 sumsq 2,
 K3 pack 4, K4 accumulate 6, K5 cast+pack 6, K6 state birth 14 (fp16 src).
-Each kernel is timed with CUDA events on the launching stream after
-warm-up; inputs >= 8M elements exceed the 126 MB L2 between iterations.
+Each kernel is timed with CUDA events around a CUDA-graph replay of
+``iters`` back-to-back launches after warm-up (device time, no host launch
+cost); inputs >= 8M elements exceed the 126 MB L2 between iterations,
+smaller ones partly hit L2.
 
     python -m paper_2108_05818_b200.microbench [--sizes 20,22,...] [--iters N]
 """
@@ -32,14 +34,23 @@ def measured_peak_gbs() -> float:
 
 
 def time_launch(fn: Callable[[], None], iters: int, warmup: int = 3) -> float:
-    """Average milliseconds per call, CUDA events on the current stream."""
+    """Average DEVICE milliseconds per call: the ``iters`` calls are captured
+    once into a CUDA graph and replayed between CUDA events, so small sizes
+    measure the kernel, not the Python/ctypes launch path."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        for _ in range(iters):
+            fn()
+    graph.replay()  # warm replay
+    torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     start.record()
-    for _ in range(iters):
-        fn()
+    graph.replay()
     end.record()
     torch.cuda.synchronize()
     return start.elapsed_time(end) / iters
