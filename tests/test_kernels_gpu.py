@@ -311,3 +311,56 @@ def test_layernorm_kernels_vs_torch_fp32(native_lib, dtype, H):
         assert (err <= 2 * ulp * ref.abs() + 4 * ulp * ref.abs().amax(dim=1, keepdim=True) * 1e-2
                 + 1e-3).all(), float(err.max())
     assert not K.layernorm_supported(128)
+
+
+def test_chunk_kernels_past_2pow31_elements(native_lib, oracle_lib):
+    """Maximum sizes: one K1 item of 2^31 + 13 elements (30 GB of state,
+    int64 tile/element indexing, ragged tail) and a K3/K5 pack at an offset
+    past 2^31 — checked against the oracle on windows at the start, across
+    the 2^31 boundary and at the end (the update is elementwise)."""
+    O = oracle_lib
+    n = (1 << 31) + 13
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 << 30:
+        pytest.skip("needs ~40 GB of free HBM")
+    g = torch.Generator(device=DEV).manual_seed(5)
+    p16 = (torch.randn(n, device=DEV, generator=g) * 1e-2).half()
+    p32 = torch.randn(n, device=DEV, generator=g) * 0.02
+    m = torch.randn(n, device=DEV, generator=g) * 1e-3
+    v = torch.rand(n, device=DEV, generator=g) * 1e-5
+    wins = [(0, 8192), ((1 << 31) - 5000, (1 << 31) + 9), (n - 3, n)]
+    before = [(_bits16(p16[a:b]), p32[a:b].cpu().numpy().copy(), m[a:b].cpu().numpy().copy(),
+               v[a:b].cpu().numpy().copy()) for a, b in wins]
+    hyper = K.AdamHyper(lr=1e-3)
+    state = K.StepState(DEV)
+    state.sumsq().fill_(1.0)
+    K.adam_prepare(state, hyper)
+    s = _oracle_state(O, state.read())
+    K.adam_chunks([(p16, p32, m, v, n)], hyper, state)
+    torch.cuda.synchronize()
+    for (a, b), (rg, rp, rm, rv) in zip(wins, before):
+        O.adam(rg, rp, rm, rv, b - a, O.FP16, 1e-3, 0.9, 0.999, 1e-8, 0.0, False, s)
+        np.testing.assert_array_equal(p32[a:b].cpu().numpy().view(np.uint32), rp.view(np.uint32))
+        np.testing.assert_array_equal(v[a:b].cpu().numpy().view(np.uint32), rv.view(np.uint32))
+        np.testing.assert_array_equal(_bits16(p16[a:b]), rg)
+    del m, v
+    # K3 / K5 at an element offset past 2^31 (chunk = the 4 GB fp16 buffer)
+    big = torch.zeros(n + 20000, dtype=torch.float16, device=DEV)
+    off = (1 << 31) + 5
+    src16 = (torch.randn(9001, device=DEV, generator=g)).half()
+    src32 = torch.randn(9001, device=DEV, generator=g)
+    K.pack([(big, off, src16, 9001)])
+    torch.cuda.synchronize()
+    assert torch.equal(big[off:off + 9001], src16)
+    K.cast_pack([(big, off + 3, src32, 9001)])
+    torch.cuda.synchronize()
+    assert torch.equal(big[off + 3:off + 3 + 9001], src32.half())
+    del big
+    # K2 over all 2^31 + 13 elements vs a float64 torch reduction
+    partials = torch.empty(K.sumsq_partials() + 1, device=DEV)
+    partials[-1:].zero_()
+    K.grad_sumsq([(p16, n)], partials[:-1])
+    st = K.StepState(DEV)
+    K.sumsq_finalize(partials, st)
+    ref = float((p16.double() ** 2).sum())
+    assert abs(float(st.sumsq().item()) - ref) <= 1e-5 * ref
