@@ -5,7 +5,10 @@ collective code is backend-agnostic, NCCL is what bench.py uses on 8 GPUs).
 Cases (reference golden ledgers): ``tiny_p2``; ``tiny_p4_tight`` (20 MiB
 budget: gathered remote chunks evicted and fetched back for the
 reduce-scatter, optimizer state split GPU/host); ``tiny_p8`` (padded tail
-group with phantom slots).
+group with phantom slots); ``tiny_p2_ckpt`` (re-gathers for RE_FWD); the
+device embedding operator with its gradient all-reduced (``tiny_p2``,
+placement "gpu"), and the host embedding operator with the asynchronous host
+Adam under ZeRO (``tiny_p4_tight``).
 
 * every rank's transfer and collective ledgers equal the REFERENCE's;
 * ZeRO with per-rank batch B trains like one rank with the concatenated
@@ -41,7 +44,7 @@ def _batches(schema, rank, n):
             for _ in range(n)]
 
 
-def _worker(rank, world, port, outdir, case):
+def _worker(rank, world, port, outdir, case, place="plan", async_adam=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -52,7 +55,9 @@ def _worker(rank, world, port, outdir, case):
         c = _case(case)
         schema = build_gpt_schema(**c["schema"])
         tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
-                          dtype=torch.float16, seed=0)
+                          dtype=torch.float16, seed=0, embedding_placement=place,
+                          untied_head=True if place != "plan" else None,
+                          async_host_adam=async_adam)
         assert tr.nproc == world and tr.rank == rank
         losses = [tr.step_host(b) for b in _batches(schema, rank, ITERS)]
         reports = [{"transfers": [[t.moment, t.chunk_id, t.src, t.dst, t.bytes, t.reason]
@@ -69,11 +74,15 @@ def _worker(rank, world, port, outdir, case):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,world", [("tiny_p2", 2), ("tiny_p4_tight", 4), ("tiny_p8", 8),
-                                        ("tiny_p2_ckpt", 2)])
-def test_multi_rank_zero_step_on_one_gpu(case, world):
+@pytest.mark.parametrize("case,world,place,async_adam", [
+    ("tiny_p2", 2, "plan", False), ("tiny_p4_tight", 4, "plan", False),
+    ("tiny_p8", 8, "plan", False), ("tiny_p2_ckpt", 2, "plan", False),
+    ("tiny_p2", 2, "gpu", False),          # device embedding operator, grads all-reduced
+    ("tiny_p4_tight", 4, "cpu", True)])    # host embedding + async host Adam under ZeRO
+def test_multi_rank_zero_step_on_one_gpu(case, world, place, async_adam):
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, 29800 + world + os.getpid() % 100, d, case),
+        port = 29800 + world * 10 + (place == "gpu") + 2 * async_adam + os.getpid() % 50 * 40
+        mp.spawn(_worker, args=(world, port, d, case, place, async_adam),
                  nprocs=world, join=True)
         res = [torch.load(os.path.join(d, "rank%d.pt" % r), weights_only=False)
                for r in range(world)]
@@ -96,7 +105,8 @@ def test_multi_rank_zero_step_on_one_gpu(case, world):
     schema2 = build_gpt_schema(**kw)
     schema1 = build_gpt_schema(**c["schema"])
     tr = ChunkTrainer(schema2, PolicySpec(**c["policy"]), HardwareSpec(gpu_count=1,
-                      gpu_bytes=180 * 10**9), dtype=torch.float16, seed=0)
+                      gpu_bytes=180 * 10**9), dtype=torch.float16, seed=0,
+                      embedding_placement=place, untied_head=True if place != "plan" else None)
     per_rank = [_batches(schema1, r, ITERS) for r in range(world)]
     single = [tr.step_host(torch.cat([per_rank[r][i] for r in range(world)]))
               for i in range(ITERS)]
