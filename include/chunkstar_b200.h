@@ -209,12 +209,14 @@ int cs_embed_bwd_host(const int64_t* tokens, int64_t n_tokens, int seq_len, cons
  * bwd: one kernel; `order` = token positions stably sorted by token id and
  * `row_start[v]..row_start[v+1]` = row v's range in it (V+1 entries, device);
  * writes every row of gwte [V,H] and gwpe [S,H] (fp32 sums in ascending token
- * order, one rounding).  Device pointers, 16-byte aligned buffers, stream-ordered. */
+ * order, one rounding); accumulate=1 adds the rounded row sums to gwte instead
+ * (K4's slot += src, for a tied LM head whose dW was written there first).
+ * Device pointers, 16-byte aligned buffers, stream-ordered. */
 int cs_embed_fwd(const int64_t* tokens, int64_t n_tokens, int seq_len, const void* wte,
                  const void* wpe, int hidden, void* out, int dtype, void* stream);
 int cs_embed_bwd(const int64_t* order, const int64_t* row_start, int64_t n_tokens, int seq_len,
                  const void* dout, int64_t vocab, int hidden, void* gwte, void* gwpe,
-                 int dtype, void* stream);
+                 int accumulate, int dtype, void* stream);
 
 /* ---- fused LM-head cross entropy (the GPT step's loss) ----------------------
  * Forward: per-row loss = logsumexp(logits_row) - logits_row[target] and the

@@ -143,3 +143,10 @@ def embed_bwd(tokens: np.ndarray, dout: np.ndarray, V: int, dtype: int):
     gp = np.zeros((S, H), dtype=np.float32)
     np.add.at(gp, np.tile(np.arange(S), B), d)
     return _narrow(gw, dtype), _narrow(gp, dtype)
+
+
+def embed_bwd_accumulate(tokens: np.ndarray, dout: np.ndarray, gwte_old: np.ndarray, dtype: int):
+    """cs_embed_bwd(accumulate=1) for wte: round(old + round(row sum)) (K4's
+    slot += src with the rounded lookup gradient as src)."""
+    gw, _ = embed_bwd(tokens, dout, gwte_old.shape[0], dtype)
+    return _narrow(_widen(gwte_old, dtype) + _widen(gw, dtype), dtype)

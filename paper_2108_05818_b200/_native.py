@@ -87,7 +87,7 @@ SIGNATURES = {
     "cs_embed_bwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
                                     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
-                                    ctypes.c_int, ctypes.c_void_p]),
+                                    ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     "cs_layernorm_supported": (ctypes.c_int, [ctypes.c_int]),
     "cs_layernorm_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,

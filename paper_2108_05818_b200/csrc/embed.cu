@@ -8,6 +8,10 @@
 //   bwd: gwte[v,:] = round(sum over tokens i with tok[i]==v, ascending i, of
 //        float(dout[i,:])), zero for rows no token hits;
 //        gwpe[s,:] = round(sum over b ascending of float(dout[b*S+s,:])).
+//   bwd with accumulate (the tied LM head already wrote its dW over wte — the
+//   grad overwrite of engine.py:177-190 — and the lookup adds to it, K4's
+//   slot += src semantics fused in): gwte[v,:] = round(float(gwte[v,:]) +
+//   float(round(sum))).
 //
 // The backward replaces a sort + segmented-reduce + scatter pipeline with ONE
 // kernel: the caller passes the token positions stably sorted by token id
@@ -82,11 +86,27 @@ __global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, int64_t n, int
   }
 }
 
+// K4 semantics fused in (accumulate): slot = round(float(slot) + float(round(sum)))
+template <int DT>
+__device__ __forceinline__ uint4 add_rounded(const uint4& old, const float* a) {
+  const uint4 r = pack8<DT>(a);
+  const uint32_t* uo = reinterpret_cast<const uint32_t*>(&old);
+  const uint32_t* ur = reinterpret_cast<const uint32_t*>(&r);
+  float f[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    f[2 * k] = __fadd_rn(to_f<DT>(uo[k] & 0xffff), to_f<DT>(ur[k] & 0xffff));
+    f[2 * k + 1] = __fadd_rn(to_f<DT>(uo[k] >> 16), to_f<DT>(ur[k] >> 16));
+  }
+  return pack8<DT>(f);
+}
+
 template <int DT>
 __global__ void embed_bwd_kernel(const int64_t* __restrict__ order,
                                  const int64_t* __restrict__ row_start, int64_t n, int S,
                                  int64_t V, int H, const uint4* __restrict__ dout,
-                                 uint4* __restrict__ gwte, uint4* __restrict__ gwpe) {
+                                 uint4* __restrict__ gwte, uint4* __restrict__ gwpe,
+                                 int accumulate) {
   const int hv = H / 8;
   const int c = threadIdx.x;
   if (c >= hv) return;
@@ -95,7 +115,8 @@ __global__ void embed_bwd_kernel(const int64_t* __restrict__ order,
   if (r < V) {
     const int64_t k0 = row_start[r], k1 = row_start[r + 1];
     for (int64_t k = k0; k < k1; ++k) acc8<DT>(a, __ldcs(dout + order[k] * hv + c));
-    gwte[r * hv + c] = pack8<DT>(a);
+    uint4* dst = gwte + r * hv + c;
+    *dst = accumulate ? add_rounded<DT>(*dst, a) : pack8<DT>(a);
   } else {
     const int64_t s = r - V;
     for (int64_t i = s; i < n; i += S) acc8<DT>(a, __ldcs(dout + i * hv + c));
@@ -147,7 +168,7 @@ extern "C" int cs_embed_fwd(const int64_t* tokens, int64_t n_tokens, int seq_len
 
 extern "C" int cs_embed_bwd(const int64_t* order, const int64_t* row_start, int64_t n_tokens,
                             int seq_len, const void* dout, int64_t vocab, int hidden,
-                            void* gwte, void* gwpe, int dtype, void* stream) {
+                            void* gwte, void* gwpe, int accumulate, int dtype, void* stream) {
   if (n_tokens < 0 || seq_len <= 0 || n_tokens % seq_len != 0 || vocab <= 0 || hidden <= 0 ||
       hidden % 8 != 0 || hidden / 8 > 1024 || !row_start || !gwte || !gwpe ||
       (n_tokens > 0 && (!order || !dout)) || (dtype != CS_FP16 && dtype != CS_BF16)) {
@@ -166,11 +187,11 @@ extern "C" int cs_embed_bwd(const int64_t* order, const int64_t* row_start, int6
   auto* gw = static_cast<uint4*>(gwte);
   auto* gp = static_cast<uint4*>(gwpe);
   if (dtype == CS_FP16)
-    embed_bwd_kernel<CS_FP16><<<(unsigned)grid, threads, 0, s>>>(order, row_start, n_tokens,
-                                                                  seq_len, vocab, hidden, d, gw, gp);
+    embed_bwd_kernel<CS_FP16><<<(unsigned)grid, threads, 0, s>>>(
+        order, row_start, n_tokens, seq_len, vocab, hidden, d, gw, gp, accumulate);
   else
-    embed_bwd_kernel<CS_BF16><<<(unsigned)grid, threads, 0, s>>>(order, row_start, n_tokens,
-                                                                  seq_len, vocab, hidden, d, gw, gp);
+    embed_bwd_kernel<CS_BF16><<<(unsigned)grid, threads, 0, s>>>(
+        order, row_start, n_tokens, seq_len, vocab, hidden, d, gw, gp, accumulate);
   cs::note_launches(1);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -255,24 +255,64 @@ class _SlotExit(torch.autograd.Function):
         return (None, None, None) + grads
 
 
+def grad_in_data(p: nn.Parameter) -> bool:
+    """True once this step's gradient was written over ``p.data`` itself (the
+    reference's grad overwrite, `engine.py:177-190`) instead of ``p.grad``;
+    the executor consumes it at ADAM and clears the mark."""
+    return getattr(p, "_cs_grad_in_data", False)
+
+
+def mark_grad_in_data(p: nn.Parameter, value: bool = True) -> None:
+    p._cs_grad_in_data = value
+
+
 class _DeviceEmbedding(torch.autograd.Function):
     """GPU-placed embedding lookup on the sm_100a kernels (cs_embed_fwd/bwd):
     the host operator's exact semantics (embedding.py), one backward kernel
-    instead of torch's sort + segmented-reduce + scatter pipeline."""
+    instead of torch's sort + segmented-reduce + scatter pipeline.  The
+    gradients are written over the weights' own storage (grad overwrite); a
+    tied LM head has already written its dW over wte, so the lookup's
+    gradient is added to it (K4 accumulate, fused into the kernel)."""
 
     @staticmethod
     def forward(ctx, tokens, wte, wpe):
         from . import kernels as K
         ctx.save_for_backward(tokens)
-        ctx.vocab, ctx.seq_rows = wte.shape[0], wpe.shape[0]
+        ctx.wte, ctx.wpe = wte, wpe
         return K.embed_fwd(tokens, wte, wpe)
 
     @staticmethod
     def backward(ctx, grad):
         from . import kernels as K
         (tokens,) = ctx.saved_tensors
-        gwte, gwpe = K.embed_bwd(tokens, grad, ctx.vocab, ctx.seq_rows)
-        return None, gwte, gwpe
+        wte, wpe = ctx.wte, ctx.wpe
+        K.embed_bwd_into(tokens, grad, wte.data, wpe.data, accumulate=grad_in_data(wte))
+        mark_grad_in_data(wte)
+        mark_grad_in_data(wpe)
+        return None, None, None
+
+
+class _LMHead(torch.autograd.Function):
+    """logits = h Wᵀ; the backward computes dh = dlogits W first and then
+    writes dW = dlogitsᵀ h over W's own storage (grad overwrite): W is not
+    read again this step (the embedding lookup's backward needs only the
+    token ids)."""
+
+    @staticmethod
+    def forward(ctx, h, w):
+        ctx.save_for_backward(h)
+        ctx.w = w
+        return F.linear(h, w)
+
+    @staticmethod
+    def backward(ctx, dlogits):
+        (h,) = ctx.saved_tensors
+        w = ctx.w
+        d2 = dlogits.reshape(-1, dlogits.shape[-1])
+        dh = torch.mm(d2, w)
+        torch.mm(d2.t(), h.reshape(-1, h.shape[-1]), out=w.data)
+        mark_grad_in_data(w)
+        return dh.view_as(h), None
 
 
 class _EmbeddingMark(torch.autograd.Function):
@@ -502,7 +542,8 @@ class ReferenceShapedGPT(nn.Module):
             h = _LNFn.apply(h)
         else:
             h = F.layer_norm(h, (self.schema.hidden_dim,))
-        logits = F.linear(h, self.wte if self.lm_head is None else self.lm_head)
+        head = self.wte if self.lm_head is None else self.lm_head
+        logits = _LMHead.apply(h, head) if self.fused else F.linear(h, head)
         if self.fused:  # sm_100a fused loss kernels (cs_xent_fwd/bwd)
             return fused_cross_entropy(logits.view(B * S, -1), targets.reshape(B * S))
         return F.cross_entropy(logits.float().view(B * S, -1), targets.reshape(B * S))

@@ -208,21 +208,32 @@ def embed_bwd(tokens: torch.Tensor, dout: torch.Tensor, vocab: int, seq_rows: in
     """(gwte [V, H], gwpe [seq_rows, H]) for the lookup's output gradient
     (cs_embed_bwd; the stable sort of the token ids is torch plumbing).
     Rows of gwpe beyond the sequence length are zero."""
-    _need_cuda(tokens, dout)
+    H = dout.shape[-1]
+    gwte = torch.empty(vocab, H, dtype=dout.dtype, device=dout.device)
+    gwpe = torch.empty(seq_rows, H, dtype=dout.dtype, device=dout.device)
+    embed_bwd_into(tokens, dout, gwte, gwpe, accumulate=False, stream=stream)
+    return gwte, gwpe
+
+
+def embed_bwd_into(tokens: torch.Tensor, dout: torch.Tensor, gwte: torch.Tensor,
+                   gwpe: torch.Tensor, accumulate: bool = False,
+                   stream: Optional[torch.cuda.Stream] = None) -> None:
+    """The lookup's gradient written over (or, ``accumulate``, added to)
+    gwte [V, H], and written over gwpe [>=S, H] (rows >= S zeroed) — e.g. the
+    weight buffers themselves (grad overwrite)."""
+    _need_cuda(tokens, dout, gwte, gwpe)
     tok = tokens.contiguous().view(-1)
     B, S = tokens.shape
-    H = dout.shape[-1]
+    V, H = gwte.shape
     d = dout.contiguous()
     srt, order = torch.sort(tok, stable=True)
-    bounds = torch.arange(vocab + 1, device=tok.device, dtype=torch.int64)
+    bounds = torch.arange(V + 1, device=tok.device, dtype=torch.int64)
     row_start = torch.searchsorted(srt, bounds)
-    gwte = torch.empty(vocab, H, dtype=dout.dtype, device=dout.device)
-    gwpe = (torch.empty(S, H, dtype=dout.dtype, device=dout.device) if seq_rows == S else
-            torch.zeros(seq_rows, H, dtype=dout.dtype, device=dout.device))
+    if gwpe.shape[0] > S:
+        gwpe[S:].zero_()
     N.check(N.load().cs_embed_bwd(order.data_ptr(), row_start.data_ptr(), B * S, S, d.data_ptr(),
-                                  vocab, H, gwte.data_ptr(), gwpe.data_ptr(),
+                                  V, H, gwte.data_ptr(), gwpe.data_ptr(), int(accumulate),
                                   _code(dout.dtype), _stream(stream)), "cs_embed_bwd")
-    return gwte, gwpe
 
 
 def sumsq_partials() -> int:

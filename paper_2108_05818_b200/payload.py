@@ -49,6 +49,7 @@ from .memory import PayloadBackend
 from .model import CPU, GPU
 from .parallel import CollectiveBackend, CommGroup, DpPartition
 from .slabs import SlabPool
+from .gpt import grad_in_data, mark_grad_in_data
 
 
 class ChunkComm:
@@ -612,11 +613,14 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._host_state = None
         emb_grads = []
         for param, _, _, _ in self.embedding:
-            if param.grad is None:
-                raise RuntimeError("embedding parameter has no gradient at ADAM")
+            # the fused model writes the gradient over the weights (grad
+            # overwrite); the plain model leaves it in .grad
+            g = param.data if grad_in_data(param) else param.grad
+            if g is None:
+                raise RuntimeError("non-chunked parameter has no gradient at ADAM")
             if self.comm is not None and self.comm.world > 1:
-                self.comm.all_reduce_avg(param.grad)
-            emb_grads.append((param.grad, param.grad.numel()))
+                self.comm.all_reduce_avg(g)
+            emb_grads.append((g, g.numel()))
         dev_items, host_items = [], []
         for pos in self.partition.local_positions(self.rank):
             chunk = cs.param_chunk(pos)
@@ -664,12 +668,15 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     done = self._transfer(self.tensor(chunk, GPU), d, GPU, CPU,
                                           self.ready.get((chunk.chunk_id, GPU)))
                     self._predrained[chunk.chunk_id] = (d, done)
-        # non-chunked embedding: its autograd gradient is packed over the
-        # parameter (K3) so it follows the same in-place update as a chunk
+        # non-chunked GPU parameters: the fused model wrote the gradient over
+        # the weights already; a plain model's autograd gradient is packed (K3)
         for param, master, m, v in self.embedding:
             flat = param.data.view(-1)
-            K.pack([(flat, 0, param.grad.view(-1), flat.numel())])
-            param.grad = None
+            if grad_in_data(param):
+                mark_grad_in_data(param, False)
+            else:
+                K.pack([(flat, 0, param.grad.view(-1), flat.numel())])
+                param.grad = None
             self._pending.append((flat, master, m, v, flat.numel()))
 
     def init_optimizer_state(self, position: int, device: str) -> None:

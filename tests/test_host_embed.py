@@ -104,3 +104,21 @@ def test_device_embedding_bit_identical_to_host_and_oracle(native_lib, oracle_li
     hw, hp = torch.empty(V, H, dtype=dtype), torch.empty(S, H, dtype=dtype)
     K.embed_bwd_host(tok, dout, hw, hp)
     assert torch.equal(hw.view(torch.int16), gw.cpu().view(torch.int16))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA GPU")
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_device_embedding_backward_accumulates_into_weights(native_lib, oracle_lib, dtype):
+    """Tied head: wte already holds the head's dW; the lookup gradient is
+    added in place (K4 semantics), wpe is overwritten, spare wpe rows zeroed."""
+    O = oracle_lib
+    B, S, V, H = 4, 32, 300, 64
+    tok, _, _, dout = _case(dtype, B, S, V, H, seed=3, repeat_tokens=True)
+    head = (torch.randn(V, H) * 0.5).to(dtype)
+    wte, wpe = head.clone().cuda(), torch.full((S + 2, H), 3.0, dtype=dtype).cuda()
+    K.embed_bwd_into(tok.cuda(), dout.cuda(), wte, wpe, accumulate=True)
+    ref = O.embed_bwd_accumulate(tok.numpy(), _bits(dout), _bits(head), CODE[dtype])
+    assert np.array_equal(_bits(wte.cpu()), ref)
+    _, rp = O.embed_bwd(tok.numpy(), _bits(dout), V, CODE[dtype])
+    assert np.array_equal(_bits(wpe[:S].cpu()), rp) and not bool(wpe[S:].any())

@@ -253,9 +253,13 @@ def test_fused_gpt_matches_unfused_gpt(native_lib):
     for fused, m in models.items():
         loss = m(tok[:, :-1], tok[:, 1:])
         (loss * 256).backward()
-        out[fused] = (loss.item(), [p.data.clone() for p in m.chunk_parameters()])
+        # chunk slots hold the dW; the fused model also writes the tied
+        # embedding/head and position gradients over wte / wpe (grad overwrite
+        # + the lookup's accumulate), the plain model leaves them in .grad
+        emb = [p.data.clone() if fused else p.grad.clone() for p in (m.wte, m.wpe)]
+        out[fused] = (loss.item(), [p.data.clone() for p in m.chunk_parameters()] + emb)
     assert abs(out[True][0] - out[False][0]) < 1e-3
-    for a, b in zip(out[True][1], out[False][1]):  # chunk slots hold the dW
+    for a, b in zip(out[True][1], out[False][1]):
         # max-norm relative error within a few fp16 ulps of the tensor's scale
         err = (a.float() - b.float()).abs().max()
         assert err <= 4e-3 * b.float().abs().max(), float(err)
