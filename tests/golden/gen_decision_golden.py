@@ -99,16 +99,21 @@ def run_rank(cs, name, skw, hkw, pkw, nproc, rank, iterations):
                                                   local_positions=local,
                                                   os_placement=policy.os_placement)
 
+    class _S:
+        pass
+    s = _S()
+    s.chunk_set, s.engine, s.dp, s.partition = chunk_set, engine, dp, partition
+    # Simulator.run's own first check (`scenario.py:141-147, 163-168`): a host
+    # too small for its shard of the layout is infeasible at moment 0
+    cpu_pool = pools[cs.model.CPU]
+    if cpu_pool.used_bytes > cpu_pool.capacity_bytes:
+        return s, [cs.engine.IterationReport(iteration=0, warmup=True, feasible=False,
+                                             failure_reason="CPU_OOM", failure_moment=0)], None
     reports = [engine.run_iteration(0, warmup=True, plan_builder=build)]
     for i in range(1, iterations):
         if not reports[-1].feasible:
             break
         reports.append(engine.run_iteration(i, warmup=False))
-
-    class _S:
-        pass
-    s = _S()
-    s.chunk_set, s.engine, s.dp, s.partition = chunk_set, engine, dp, partition
     return s, reports, engine.plan
 
 
