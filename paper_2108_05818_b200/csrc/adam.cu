@@ -32,7 +32,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kGroups = 4;   // 4-element groups per thread per block tile (K2)
-constexpr int kBlockTile = kThreads * kGroups * 4;
+constexpr int kSumsqTile = kThreads * kGroups * 8;  // K2: 128-bit groups
 // K1 tiling variants (groups per thread, min resident CTAs per SM -> register
 // cap).  Selected once per process (CS_ADAM_VARIANT, default kAdamDefault);
 // every variant computes bit-identical results.
@@ -220,23 +220,26 @@ grad_sumsq_kernel(const __grid_constant__ GradBatch b, float* __restrict__ parti
   for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
     const int k = find_item(b.tile_start, b.n, tile);
     const CsGradItem it = b.item[k];
-    const int64_t base = (tile - b.tile_start[k]) * kBlockTile;
+    const int64_t base = (tile - b.tile_start[k]) * kSumsqTile;
     const uint16_t* __restrict__ g16 = static_cast<const uint16_t*>(it.g16);
-    if (base + kBlockTile <= it.n) {
-      uint2 g[kGroups];
+    if (base + kSumsqTile <= it.n && (reinterpret_cast<uintptr_t>(g16) & 15) == 0) {
+      // four 128-bit loads in flight per thread before any math
+      uint4 g[kGroups];
 #pragma unroll
       for (int u = 0; u < kGroups; ++u)
-        g[u] = __ldcs(reinterpret_cast<const uint2*>(
-            g16 + base + (int64_t)(u * kThreads + threadIdx.x) * 4));
+        g[u] = __ldcs(reinterpret_cast<const uint4*>(
+            g16 + base + (int64_t)(u * kThreads + threadIdx.x) * 8));
 #pragma unroll
       for (int u = 0; u < kGroups; ++u) {
-        const float4 f = widen4<DT>(g[u]);
+        const float4 f = widen4<DT>(make_uint2(g[u].x, g[u].y));
+        const float4 h = widen4<DT>(make_uint2(g[u].z, g[u].w));
         acc += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+        acc += h.x * h.x + h.y * h.y + h.z * h.z + h.w * h.w;
       }
     } else {
       for (int u = 0; u < kGroups; ++u) {
-        const int64_t e0 = base + (int64_t)(u * kThreads + threadIdx.x) * 4;
-        for (int64_t e = e0; e < e0 + 4 && e < it.n; ++e) {
+        const int64_t e0 = base + (int64_t)(u * kThreads + threadIdx.x) * 8;
+        for (int64_t e = e0; e < e0 + 8 && e < it.n; ++e) {
           const float f = widen1<DT>(g16[e]);
           acc += f * f;
         }
@@ -492,7 +495,7 @@ extern "C" int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
       if (it.n == 0) continue;
       b.item[b.n] = it;
       b.tile_start[b.n] = tiles;
-      tiles += (it.n + kBlockTile - 1) / kBlockTile;
+      tiles += (it.n + kSumsqTile - 1) / kSumsqTile;
       ++b.n;
     }
     b.tile_start[b.n] = tiles;
