@@ -368,3 +368,27 @@ def test_reference_criterion_06_volume_identity_on_the_real_step():
     assert len(roomy.sim.engine.plan.os_positions_on_gpu) == roomy.sim.chunk_set.positions
     for r in roomy.reports[1:]:
         assert sum(t.bytes for t in r.transfers if t.reason == "adam_copy") == 0
+
+
+@pytest.mark.parametrize("ckpt,dtype", [(True, torch.float16), (False, torch.bfloat16)])
+def test_cuda_graph_replay_with_checkpointing_and_bf16(ckpt, dtype):
+    """Graph replay of the steady state also covers the recomputing
+    (activation-checkpointed) step and bf16 chunks: bit-identical to eager."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_cap256Ki"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 7)
+    out = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for graph in (False, True):
+            tr = ChunkTrainer(schema, PolicySpec(**dict(c["policy"], checkpointing=ckpt)),
+                              HardwareSpec(**c["hardware"]), dtype=dtype, seed=0,
+                              cuda_graph=graph, embedding_placement="gpu")
+            losses = [tr.step_host(t) for t in toks]
+            out[graph] = (losses, [tr.local_chunk_payload(p).cpu().clone()
+                                   for p in range(tr.sim.chunk_set.positions)], tr)
+    assert out[True][2]._graph is not None
+    assert out[True][0] == out[False][0]
+    for a, b in zip(out[True][1], out[False][1]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
