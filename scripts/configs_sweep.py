@@ -35,6 +35,8 @@ CONFIGS = {
     "12b_ckpt": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI, os="auto",
                      ckpt=True),
     "12b_mixed": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI, os="auto"),
+    "12b_mixed_85": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI, os="auto",
+                         gpu_frac=0.85),
     "1b_b16_emb_plan": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
                             os="auto"),
     "1b_b16_emb_gpu": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
@@ -52,9 +54,16 @@ def run_one(name: str) -> dict:
     schema = build_gpt_schema(layers=c["layers"], hidden_dim=c["hidden"], heads=c["heads"],
                               seq_len=1024, vocab=50304, batch=c["batch"])
     t_init = time.perf_counter()
+    hw = None
+    if "gpu_frac" in c:  # accounting budget as a fraction of HBM (trainer default 0.9)
+        from paper_2108_05818_b200.config import HardwareSpec
+        total = torch.cuda.get_device_properties(0).total_memory
+        hw = HardwareSpec(gpu_count=1, gpu_bytes=int(total * c["gpu_frac"]),
+                          cpu_bytes=int(0.8 * os.sysconf("SC_PAGE_SIZE") *
+                                        os.sysconf("SC_PHYS_PAGES")))
     tr = ChunkTrainer(schema, PolicySpec(capacity_elems=c["cap"], os_placement=c["os"],
                                          checkpointing=c.get("ckpt", False)),
-                      seed=0, hyper=K.AdamHyper(lr=1e-4), cuda_graph=True,
+                      hardware=hw, seed=0, hyper=K.AdamHyper(lr=1e-4), cuda_graph=True,
                       embedding_placement=c.get("emb", "plan"), untied_head=c.get("untied"))
     t_init = time.perf_counter() - t_init
     gen = torch.Generator().manual_seed(3)
@@ -77,7 +86,12 @@ def run_one(name: str) -> dict:
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / steps
     hs1 = torch.cuda.host_memory_stats()
-    retries = torch.cuda.memory_stats().get("num_alloc_retries", 0) - retries0
+    ms1 = torch.cuda.memory_stats()
+    retries = ms1.get("num_alloc_retries", 0) - retries0
+    dev_alloc = {k: ms1.get(k) for k in ("num_device_alloc", "num_device_free", "num_ooms",
+                                        "reserved_bytes.all.peak", "allocated_bytes.all.peak",
+                                        "inactive_split_bytes.all.peak")}
+    free_b, total_b = torch.cuda.mem_get_info()
     host_phase_ms = {k: round((tr.phase_seconds[k] - ph0[k]) * 1e3 / steps, 1) for k in ph0}
     pinned = {k: hs1[k] - hs0.get(k, 0) for k in hs1
               if isinstance(hs1[k], (int, float)) and hs1[k] != hs0.get(k, 0)}
@@ -100,6 +114,9 @@ def run_one(name: str) -> dict:
             "checkpointing": bool(c.get("ckpt", False)),
             "host_phase_ms_per_step": host_phase_ms,
             "cuda_alloc_retries_during_timing": retries,
+            "device_allocator": dev_alloc, "mem_get_info_end": [free_b, total_b],
+            "slab_pool": {"allocs": tr.executor.slabs.allocs, "reuses": tr.executor.slabs.reuses,
+                          "slab_bytes": tr.executor.slabs.slab_bytes},
             "alloc_conf": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", ""), "pinned_alloc_during_timing": pinned,
             "pinned_stats_end": {k: v for k, v in hs1.items() if "current" in k or "peak" in k},
             "embedding_device": tr.embedding_placement,
