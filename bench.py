@@ -168,6 +168,7 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
                           generator=gen).to(dev) for _ in range(2)]
     for i in range(warmup):
         tr.step(toks[i % 2])
+    tr.finish_host_work()  # the warm-up's last host updates are not timed
     torch.cuda.synchronize()
     st = tr.executor.stats
     st.copy_events.clear()

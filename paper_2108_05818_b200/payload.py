@@ -165,11 +165,12 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._host_state = None
         self._state_snap = None
         #: run host Adam of CPU-placed positions on a worker thread, overlapping
-        #: the main thread's enqueue of the rest of the step and the next one.
-        #: Opt-in: bit-identical, but at 1B with every triplet on the host it
-        #: measured within noise of the synchronous walk (365-385 vs 368-370
-        #: ms/step) — the host Adam slows down by as much as it overlaps.
-        self.async_host_adam = os.environ.get("CS_ASYNC_HOST_ADAM", "0") == "1"
+        #: the main thread's enqueue of the rest of the step and the next
+        #: forward (bit-identical).  12B with 58 host-placed positions: 2.05-2.62
+        #: vs 2.28-2.81 s/step; 1B with every triplet on the host: within noise
+        #: (the host Adam slows down by what it overlaps).  CS_ASYNC_HOST_ADAM=0
+        #: restores the synchronous walk.
+        self.async_host_adam = os.environ.get("CS_ASYNC_HOST_ADAM", "1") != "0"
         self._worker: Optional[ThreadPoolExecutor] = None
         self._jobs: Dict[int, _HostAdamJob] = {}   # chunk id -> unfinished job
         self._stats_lock = threading.Lock()
