@@ -38,8 +38,8 @@ constexpr int kSumsqTile = kThreads * kGroups * 8;  // K2: 128-bit groups
 // every variant computes bit-identical results.
 struct AdamVariant { int groups, min_blocks; };
 constexpr AdamVariant kAdamVariants[] = {{4, 1}, {4, 4}, {2, 4}, {2, 6}, {8, 2}};
-constexpr int kAdamSimtVariants = 5;   // 5..7 = TMA-staged variants (adam_tma.cu)
-constexpr int kAdamVariantCount = 16;
+constexpr int kAdamSimtVariants = 5;   // 5..17 = TMA-staged variants (adam_tma.cu)
+constexpr int kAdamVariantCount = 18;
 constexpr int kAdamDefault = 12;  // TMA-staged, 16 consumer warps, 4096 x 3 stages
 
 struct AdamBatch {
@@ -412,7 +412,7 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
       }
       return cs_adam_chunks_tma(items, n_items, dtype, hyper, d_state, stream, variant);
     }
-    variant = kAdamDefault;  // bulk copies need 16-byte aligned streams
+    variant = 0;  // bulk copies need 16-byte aligned streams: the SIMT kernel takes the rest
   }
   const int64_t tile_elems = (int64_t)kThreads * kAdamVariants[variant].groups * 4;
   AdamKernel kern = dtype == CS_FP16 ? adam_kernel_for<CS_FP16>(variant)

@@ -239,7 +239,7 @@ adam_tma_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict__
 // store warp (bulk stores).  Consumers publish a finished stage by arriving on
 // computed[s] (count = all consumer threads) and move straight on; only the
 // store warp waits for the bulk reads before freeing the stage.
-template <int DT, int T, int STAGES, int CW>
+template <int DT, int T, int STAGES, int CW, int U = 1>
 __global__ void __launch_bounds__(CW * 32 + 64)
 adam_tma3_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict__ st) {
   constexpr int kConsumerWarps = CW;
@@ -325,21 +325,57 @@ adam_tma3_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict_
     float* m = reinterpret_cast<float*>(base + T * 6);
     float* v = reinterpret_cast<float*>(base + T * 10);
     mbar_wait(&full[s], phase);
-    for (int e = t * 4; e < len; e += kConsumers * 4) {
-      uint2 gw = *reinterpret_cast<uint2*>(g16 + e);
-      float4 pp = *reinterpret_cast<float4*>(p + e);
-      float4 mm = *reinterpret_cast<float4*>(m + e);
-      float4 vv = *reinterpret_cast<float4*>(v + e);
-      adam1(to_f<DT>(gw.x & 0xffff), pp.x, mm.x, vv.x, c);
-      adam1(to_f<DT>(gw.x >> 16), pp.y, mm.y, vv.y, c);
-      adam1(to_f<DT>(gw.y & 0xffff), pp.z, mm.z, vv.z, c);
-      adam1(to_f<DT>(gw.y >> 16), pp.w, mm.w, vv.w, c);
-      *reinterpret_cast<float4*>(p + e) = pp;
-      *reinterpret_cast<float4*>(m + e) = mm;
-      *reinterpret_cast<float4*>(v + e) = vv;
-      gw.x = (uint32_t)from_f<DT>(pp.x) | ((uint32_t)from_f<DT>(pp.y) << 16);
-      gw.y = (uint32_t)from_f<DT>(pp.z) | ((uint32_t)from_f<DT>(pp.w) << 16);
-      *reinterpret_cast<uint2*>(g16 + e) = gw;
+    if (U == 1) {
+      for (int e = t * 4; e < len; e += kConsumers * 4) {
+        uint2 gw = *reinterpret_cast<uint2*>(g16 + e);
+        float4 pp = *reinterpret_cast<float4*>(p + e);
+        float4 mm = *reinterpret_cast<float4*>(m + e);
+        float4 vv = *reinterpret_cast<float4*>(v + e);
+        adam1(to_f<DT>(gw.x & 0xffff), pp.x, mm.x, vv.x, c);
+        adam1(to_f<DT>(gw.x >> 16), pp.y, mm.y, vv.y, c);
+        adam1(to_f<DT>(gw.y & 0xffff), pp.z, mm.z, vv.z, c);
+        adam1(to_f<DT>(gw.y >> 16), pp.w, mm.w, vv.w, c);
+        *reinterpret_cast<float4*>(p + e) = pp;
+        *reinterpret_cast<float4*>(m + e) = mm;
+        *reinterpret_cast<float4*>(v + e) = vv;
+        gw.x = (uint32_t)from_f<DT>(pp.x) | ((uint32_t)from_f<DT>(pp.y) << 16);
+        gw.y = (uint32_t)from_f<DT>(pp.z) | ((uint32_t)from_f<DT>(pp.w) << 16);
+        *reinterpret_cast<uint2*>(g16 + e) = gw;
+      }
+    } else {
+      // U groups of 4 per thread per pass: every smem load issued before the
+      // math, U*4 independent update chains for the schedulers (low-clock ILP)
+      for (int e0 = t * 4; e0 < len; e0 += kConsumers * 4 * U) {
+        uint2 gw[U];
+        float4 pp[U], mm[U], vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kConsumers * 4;
+          if (e < len) {
+            gw[u] = *reinterpret_cast<uint2*>(g16 + e);
+            pp[u] = *reinterpret_cast<float4*>(p + e);
+            mm[u] = *reinterpret_cast<float4*>(m + e);
+            vv[u] = *reinterpret_cast<float4*>(v + e);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kConsumers * 4;
+          if (e < len) {
+            adam1(to_f<DT>(gw[u].x & 0xffff), pp[u].x, mm[u].x, vv[u].x, c);
+            adam1(to_f<DT>(gw[u].x >> 16), pp[u].y, mm[u].y, vv[u].y, c);
+            adam1(to_f<DT>(gw[u].y & 0xffff), pp[u].z, mm[u].z, vv[u].z, c);
+            adam1(to_f<DT>(gw[u].y >> 16), pp[u].w, mm[u].w, vv[u].w, c);
+            *reinterpret_cast<float4*>(p + e) = pp[u];
+            *reinterpret_cast<float4*>(m + e) = mm[u];
+            *reinterpret_cast<float4*>(v + e) = vv[u];
+            uint2 o;
+            o.x = (uint32_t)from_f<DT>(pp[u].x) | ((uint32_t)from_f<DT>(pp[u].y) << 16);
+            o.y = (uint32_t)from_f<DT>(pp[u].z) | ((uint32_t)from_f<DT>(pp[u].w) << 16);
+            *reinterpret_cast<uint2*>(g16 + e) = o;
+          }
+        }
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive(&computed[s]);
@@ -359,14 +395,14 @@ adam_tma3_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict_
   }
 }
 
-template <int DT, int T, int STAGES, bool THREE = false, int CW = 8>
+template <int DT, int T, int STAGES, bool THREE = false, int CW = 8, int U = 1>
 int launch(const CsAdamItem* items, int n_items, const CsAdamHyper* h,
            const CsStepState* d_state, cudaStream_t stream, int ctas_per_sm) {
   constexpr int kSmem = STAGES * T * 14 + 3 * STAGES * 8;
   static bool configured = false;
   if (!configured) {
     if (THREE)
-      cudaFuncSetAttribute(adam_tma3_kernel<DT, T, STAGES, CW>,
+      cudaFuncSetAttribute(adam_tma3_kernel<DT, T, STAGES, CW, U>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     else
       cudaFuncSetAttribute(adam_tma_kernel<DT, T, STAGES>,
@@ -399,7 +435,7 @@ int launch(const CsAdamItem* items, int n_items, const CsAdamHyper* h,
     const int64_t need = tiles > b.n ? tiles : b.n;  // every item's tail needs a CTA
     if (grid > need) grid = need;
     if (THREE)
-      adam_tma3_kernel<DT, T, STAGES, CW><<<(int)grid, CW * 32 + 64, kSmem, stream>>>(b, d_state);
+      adam_tma3_kernel<DT, T, STAGES, CW, U><<<(int)grid, CW * 32 + 64, kSmem, stream>>>(b, d_state);
     else
       adam_tma_kernel<DT, T, STAGES><<<(int)grid, kThreads, kSmem, stream>>>(b, d_state);
     cs::note_launches(1);
@@ -425,6 +461,16 @@ int cs_adam_chunks_tma(const CsAdamItem* items, int n_items, int dtype, const Cs
     if (dtype == CS_FP16)
       return cs_tma::launch<CS_FP16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
     return cs_tma::launch<CS_BF16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 16) {  // variant 12 with two 4-element groups per consumer pass
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 4096, 3, true, 16, 2>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 4096, 3, true, 16, 2>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 17) {  // 8 consumer warps, two groups per pass, 4096 x 3 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 4096, 3, true, 8, 2>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 4096, 3, true, 8, 2>(items, n_items, h, d_state, s, 1);
   }
   if (variant == 12) {  // 16 consumer warps, 4096 x 3 stages
     if (dtype == CS_FP16)

@@ -34,7 +34,8 @@ def _oracle_state(O, st: "K.N.CsStepState"):
     return s
 
 
-@pytest.fixture(params=[0, 2, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15], ids=lambda v: "variant%d" % v)
+@pytest.fixture(params=[0, 2, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17],
+                ids=lambda v: "variant%d" % v)
 def adam_variant(request, native_lib):
     old = native_lib.cs_adam_variant(-1)
     native_lib.cs_adam_variant(request.param)
@@ -368,3 +369,29 @@ def test_chunk_kernels_past_2pow31_elements(native_lib, oracle_lib):
     K.sumsq_finalize(partials, st)
     ref = float((p16.double() ** 2).sum())
     assert abs(float(st.sumsq().item()) - ref) <= 1e-5 * ref
+
+
+def test_adam_chunks_8_byte_aligned_items_take_the_simt_path(native_lib, oracle_lib):
+    """The TMA variants need 16-byte aligned streams; an fp16 view offset by
+    8 bytes is routed to the SIMT kernel (same bits), not rejected."""
+    O = oracle_lib
+    n = 70001
+    g = torch.Generator().manual_seed(4)
+    base16 = (torch.randn(n + 4, generator=g) * 1e-2).half()
+    p = torch.randn(n, generator=g) * 0.02
+    m = torch.randn(n, generator=g) * 1e-3
+    v = torch.rand(n, generator=g) * 1e-5
+    hyper = K.AdamHyper(lr=1e-3)
+    state = K.StepState(DEV)
+    state.sumsq().fill_(1.0)
+    K.adam_prepare(state, hyper)
+    s = _oracle_state(O, state.read())
+    d16 = base16.to(DEV)[4:]            # data_ptr % 16 == 8
+    assert d16.data_ptr() % 16 == 8
+    dp, dm, dv = p.to(DEV), m.to(DEV), v.to(DEV)
+    rg, rp, rm, rv = _bits16(base16[4:]), p.numpy().copy(), m.numpy().copy(), v.numpy().copy()
+    K.adam_chunks([(d16, dp, dm, dv, n)], hyper, state)
+    torch.cuda.synchronize()
+    O.adam(rg, rp, rm, rv, n, O.FP16, 1e-3, 0.9, 0.999, 1e-8, 0.0, False, s)
+    np.testing.assert_array_equal(dp.cpu().numpy().view(np.uint32), rp.view(np.uint32))
+    np.testing.assert_array_equal(_bits16(d16), rg)
