@@ -30,7 +30,9 @@
  *     v  = fma(c2 * g, g, v * b2)                 (mul_ + addcmul_)
  *     p  = p + ((-s.step_size) * m) / (sqrt(v) / s.sqrt_bc2 + eps)
  *     p16 = round_to_nearest_even(p)
- * When s.skip != 0 (non-finite gradients) nothing is written.
+ * When s.skip != 0 (non-finite gradients) p32 / m / v are not written and
+ * p16 = round(p32): the 16-bit chunk held the step's gradients (grad
+ * overwrite), so the unchanged parameters are put back over them.
  */
 #ifndef CHUNKSTAR_B200_H
 #define CHUNKSTAR_B200_H

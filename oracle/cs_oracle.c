@@ -152,7 +152,13 @@ void or_adam_prepare(OrStepState* s, double lr, double beta1, double beta2, floa
 void or_adam(uint16_t* p16, float* p32, float* m, float* v, int64_t n, int dtype,
              double lr, double beta1, double beta2, double eps, double wd, int adamw,
              const OrStepState* s, int n_threads) {
-  if (s->skip) return;
+  if (s->skip) {
+    /* skipped step (non-finite gradients): p32 / m / v stay, but the 16-bit
+     * chunk holds this step's gradients (grad overwrite) — put the unchanged
+     * parameters back over them */
+    for (int64_t i = 0; i < n; ++i) p16[i] = narrow(p32[i], dtype);
+    return;
+  }
   /* scalars formed in double, rounded once (torch.optim.Adam passes python
    * floats to its float kernels the same way) */
   const float b2 = (float)beta2, omb1 = (float)(1.0 - beta1), omb2 = (float)(1.0 - beta2);

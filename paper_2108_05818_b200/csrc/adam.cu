@@ -121,6 +121,24 @@ __device__ __forceinline__ void adam1(float g16, float& p, float& m, float& v,
   p = __fadd_rn(p, __fdiv_rn(__fmul_rn(c.neg_step_size, m), denom));
 }
 
+// A skipped step (non-finite gradients) leaves p32 / m / v untouched, but the
+// 16-bit chunk holds the step's gradients (the grad overwrite of
+// engine.py:177-190): every element gets its unchanged parameter back,
+// p16 = round(p32).  Grid-stride over all items; rare, so plain loads.
+template <int DT>
+__device__ void restore_params(const CsAdamItem* items, int n_items, const CsStepState* st) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int i = 0; i < n_items; ++i) {
+    const CsAdamItem it = items[i];
+    uint16_t* q16 = static_cast<uint16_t*>(it.p16);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < it.n; e += stride) {
+      const float f = it.p32[e];
+      q16[e] = DT == CS_FP16 ? __half_as_ushort(__float2half_rn(f))
+                             : __bfloat16_as_ushort(__float2bfloat16_rn(f));
+    }
+  }
+}
+
 __device__ __forceinline__ int find_item(const int64_t* start, int n, int64_t tile) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -134,7 +152,10 @@ template <int DT, int G, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
 adam_chunks_kernel(const __grid_constant__ AdamBatch b, const CsStepState* __restrict__ st) {
   constexpr int kTile = kThreads * G * 4;
-  if (st->skip) return;  // non-finite gradients: the whole step is skipped
+  if (st->skip) {  // non-finite gradients: no update, parameters restored
+    restore_params<DT>(b.item, b.n, st);
+    return;
+  }
   AdamConsts c;
   c.grad_scale = st->grad_scale;
   c.neg_step_size = -st->step_size;

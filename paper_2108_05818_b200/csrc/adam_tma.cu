@@ -127,7 +127,16 @@ adam_tma_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict__
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
   uint64_t* empty = full + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (st->skip) return;
+  if (st->skip) {  // non-finite gradients: no update, p16 = round(p32) restored
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int i = 0; i < b.n; ++i) {
+      const CsAdamItem it = b.item[i];
+      uint16_t* q16 = static_cast<uint16_t*>(it.p16);
+      for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < it.n; e += stride)
+        q16[e] = from_f<DT>(it.p32[e]);
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -250,7 +259,16 @@ adam_tma3_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict_
   uint64_t* empty = full + STAGES;
   uint64_t* computed = empty + STAGES;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (st->skip) return;
+  if (st->skip) {  // non-finite gradients: no update, p16 = round(p32) restored
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int i = 0; i < b.n; ++i) {
+      const CsAdamItem it = b.item[i];
+      uint16_t* q16 = static_cast<uint16_t*>(it.p16);
+      for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < it.n; e += stride)
+        q16[e] = from_f<DT>(it.p32[e]);
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);

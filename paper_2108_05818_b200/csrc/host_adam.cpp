@@ -88,6 +88,23 @@ __attribute__((target("avx2,fma,f16c"))) void adam_range(const CsAdamItem& it, i
   }
 }
 
+// A skipped step leaves p32 / m / v alone, but the 16-bit chunk holds the
+// step's gradients (grad overwrite): put the unchanged parameters back.
+template <int DT>
+__attribute__((target("avx2,fma,f16c"))) void restore_item(const CsAdamItem& it, int threads) {
+  if (it.n <= 0) return;
+  uint16_t* q16 = static_cast<uint16_t*>(it.p16);
+  const int64_t nv = it.n & ~(int64_t)7;
+#pragma omp parallel for num_threads(threads) schedule(static)
+  for (int64_t e = 0; e < nv; e += 8) store16<DT>(q16 + e, _mm256_loadu_ps(it.p32 + e));
+  for (int64_t e = nv; e < it.n; ++e) {
+    alignas(32) float t[8] = {it.p32[e]};
+    alignas(16) uint16_t o[8];
+    store16<DT>(o, _mm256_load_ps(t));
+    q16[e] = o[0];
+  }
+}
+
 __attribute__((target("avx2,fma,f16c"))) Consts make_consts(const CsAdamHyper& h,
                                                          const CsStepState& s) {
   // scalars formed in double and rounded once, exactly as cs_adam_chunks
@@ -121,7 +138,13 @@ extern "C" int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dty
     cs::set_error("cs_adam_chunks_host: host CPU lacks AVX2/FMA/F16C");
     return CS_EINVAL;
   }
-  if (state->skip) return 0;
+  if (state->skip) {  // non-finite gradients: no update, p16 = round(p32) restored
+    const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+    for (int i = 0; i < n_items; ++i)
+      if (dtype == CS_FP16) restore_item<CS_FP16>(items[i], threads);
+      else restore_item<CS_BF16>(items[i], threads);
+    return 0;
+  }
   const Consts c = make_consts(*hyper, *state);
   constexpr int64_t kRange = 1 << 16;
   std::vector<std::pair<int, int64_t>> ranges;

@@ -51,11 +51,25 @@ def test_host_adam_bit_exact_vs_oracle(native_lib, oracle_lib, dtype, wd, adamw)
         np.testing.assert_array_equal(g.view(torch.int16).numpy().view(np.uint16), rg)
 
 
-def test_host_adam_respects_skip(native_lib):
-    g = torch.ones(16, dtype=torch.float16)
-    p = torch.zeros(16)
-    m, v = torch.zeros(16), torch.zeros(16)
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_host_adam_skip_restores_params(native_lib, oracle_lib, dtype):
+    """Skipped step: p32 / m / v untouched, p16 (holding the overflowed
+    gradients) gets round(p32) back — same bits as the oracle, ragged tail."""
+    O = oracle_lib
+    n = 8 * 1000 + 5
+    gen = torch.Generator().manual_seed(6)
+    g = torch.full((n,), float("inf")).to(dtype)
+    p = torch.randn(n, generator=gen)
+    m, v = torch.randn(n, generator=gen), torch.rand(n, generator=gen)
+    ref = (g.view(torch.int16).numpy().view(np.uint16).copy(), p.numpy().copy(),
+           m.numpy().copy(), v.numpy().copy())
     s = N.CsStepState()
     s.skip = 1
-    K.adam_chunks_host([(g, p, m, v, 16)], K.AdamHyper(), s)
-    assert (g == 1).all() and (p == 0).all()
+    K.adam_chunks_host([(g, p, m, v, n)], K.AdamHyper(), s, n_threads=3)
+    so = O.step_state(1.0)
+    so.skip = 1
+    O.adam(*ref, n, O.FP16 if dtype == torch.float16 else O.BF16, 1e-4, 0.9, 0.999, 1e-8, 0.0,
+           False, so)
+    assert np.array_equal(p.numpy(), ref[1]) and np.array_equal(m.numpy(), ref[2])
+    assert np.array_equal(g.view(torch.int16).numpy().view(np.uint16), ref[0])
+    assert torch.equal(g, p.to(dtype))

@@ -103,20 +103,36 @@ def test_adam_chunks_many_items_and_prefix_only(native_lib, oracle_lib, adam_var
         np.testing.assert_array_equal(_bits16(c[0])[used:], tail[0])
 
 
-def test_adam_skip_leaves_state_untouched(native_lib, adam_variant):
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_adam_skip_restores_params_and_leaves_state(native_lib, oracle_lib, adam_variant, dtype):
+    """Skipped step (non-finite gradients): p32 / m / v untouched, and the
+    16-bit chunk — which holds the step's (overflowed) gradients under the
+    grad overwrite — gets the unchanged parameters back, p16 = round(p32);
+    same bits as the oracle.  Ragged sizes, several items."""
+    O = oracle_lib
     hyper = K.AdamHyper()
     state = K.StepState(DEV, init_loss_scale=65536.0)
     state.sumsq().fill_(float("inf"))
     K.adam_prepare(state, hyper, dynamic_scale=True)
     st = state.read()
     assert st.skip == 1 and st.step == 0 and st.loss_scale == 32768.0
-    p16 = torch.full((1000,), float("inf"), dtype=torch.float16, device=DEV)
-    p32 = torch.ones(1000, device=DEV)
-    m = torch.zeros(1000, device=DEV)
-    v = torch.zeros(1000, device=DEV)
-    K.adam_chunks([(p16, p32, m, v, 1000)], hyper, state)
+    g = torch.Generator().manual_seed(8)
+    items, refs = [], []
+    for n in (1, 1000, 4099, 70001):
+        p32 = torch.randn(n, generator=g)
+        p16 = torch.full((n,), float("inf"), dtype=dtype)
+        m, v = torch.randn(n, generator=g), torch.rand(n, generator=g)
+        refs.append((_bits16(p16), p32.numpy().copy(), m.numpy().copy(), v.numpy().copy()))
+        items.append((p16.to(DEV), p32.to(DEV), m.to(DEV), v.to(DEV), n))
+    K.adam_chunks(items, hyper, state)
     torch.cuda.synchronize()
-    assert (p32 == 1).all() and (m == 0).all() and torch.isinf(p16).all()
+    s = _oracle_state(O, st)
+    for (d16, d32, dm, dv, n), (r16, r32, rm, rv) in zip(items, refs):
+        O.adam(r16, r32, rm, rv, n, _code(O, dtype), 1e-4, 0.9, 0.999, 1e-8, 0.0, False, s)
+        assert np.array_equal(d32.cpu().numpy(), r32) and np.array_equal(dm.cpu().numpy(), rm)
+        assert np.array_equal(dv.cpu().numpy(), rv)
+        assert np.array_equal(_bits16(d16), r16)
+        assert torch.equal(d16.cpu(), d32.cpu().to(dtype))  # the parameters are back
 
 
 def test_grad_sumsq_and_step_scalars_match_oracle(native_lib, oracle_lib):

@@ -392,3 +392,33 @@ def test_cuda_graph_replay_with_checkpointing_and_bf16(ckpt, dtype):
     assert out[True][0] == out[False][0]
     for a, b in zip(out[True][1], out[False][1]):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+@pytest.mark.parametrize("case", ["tiny_cap256Ki", "tiny_tight"])
+def test_overflow_steps_are_skipped_without_touching_the_model(case):
+    """Dynamic loss scaling from an absurd scale: the first steps overflow and
+    are skipped.  A skipped step must leave the model exactly as it was —
+    the fp16 chunks, which hold the step's gradients under the grad
+    overwrite, get their parameters back — so the same batch gives the same
+    loss until the scale has backed off, and training then proceeds."""
+    from paper_2108_05818_b200.chunks import ChunkKind
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES[case]
+    schema = build_gpt_schema(**c["schema"])
+    tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                      dtype=torch.float16, seed=0, init_loss_scale=2.0 ** 26,
+                      dynamic_loss_scale=True)
+    batch = _tokens(schema, 1)[0]
+    losses = [tr.step_host(batch) for _ in range(16)]
+    tr.finish_host_work()
+    st = tr.step_state()
+    skipped = 16 - int(st.step)
+    assert 2 <= skipped < 16 and st.loss_scale < 2.0 ** 26, (skipped, st.loss_scale)
+    assert all(np.isfinite(losses)), losses
+    assert len(set(losses[:skipped])) == 1, losses[:skipped + 1]   # the model did not move
+    assert losses[-1] < losses[0]
+    for pos in range(tr.sim.chunk_set.positions):                  # p16 == round(p32)
+        n = tr.sim.chunk_set.param_chunk(pos).used_elems
+        p16 = tr.local_chunk_payload(pos)[:n].cpu()
+        p32 = tr.local_chunk_payload(pos, ChunkKind.PARAM_FP32)[:n].cpu()
+        assert torch.equal(p16, p32.half())
