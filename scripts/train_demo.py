@@ -34,6 +34,13 @@ def main():
                     help="tokens the chain visits (a random subset of the vocabulary)")
     ap.add_argument("--lr", type=float, default=3e-4)
     ap.add_argument("--every", type=int, default=25)
+    ap.add_argument("--os", default="auto", choices=["auto", "cpu", "gpu"],
+                    help="optimizer-state placement policy")
+    ap.add_argument("--gpu-gb", type=float, default=0.0,
+                    help="accounting GPU budget in GB (0: 90%% of HBM) — small values evict")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="deterministic attention backend (bit-comparable runs)")
+    ap.add_argument("--no-graph", action="store_true")
     a = ap.parse_args()
     import torch
     from paper_2108_05818_b200 import kernels as K
@@ -55,8 +62,15 @@ def main():
 
     schema = build_gpt_schema(layers=a.layers, hidden_dim=a.hidden, heads=a.heads,
                               seq_len=a.seq, vocab=a.vocab, batch=a.batch)
-    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=64 << 20), seed=0,
-                      hyper=K.AdamHyper(lr=a.lr, betas=(0.9, 0.95)), cuda_graph=True)
+    from paper_2108_05818_b200.config import HardwareSpec
+    hw = (HardwareSpec(gpu_count=1, gpu_bytes=int(a.gpu_gb * 1e9), cpu_bytes=150 * 10 ** 9)
+          if a.gpu_gb else None)
+    cap = 64 << 20 if a.hidden >= 2048 else 4 * a.hidden * a.hidden
+    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=cap, os_placement=a.os), hw, seed=0,
+                      hyper=K.AdamHyper(lr=a.lr, betas=(0.9, 0.95)), cuda_graph=not a.no_graph)
+    if a.deterministic:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        sdpa_kernel(SDPBackend.MATH).__enter__()
     t0 = time.perf_counter()
     losses = []
     for i in range(a.steps):
@@ -76,7 +90,10 @@ def main():
                       "ln_successors_floor": round(math.log(a.succ), 4),
                       "skipped_steps": a.steps - int(st.step), "final_loss_scale": st.loss_scale,
                       "wall_s": round(time.perf_counter() - t0, 1),
-                      "all_finite": all(math.isfinite(x) for x in losses)}), flush=True)
+                      "all_finite": all(math.isfinite(x) for x in losses),
+                      "host_adam_items": tr.executor.stats.host_adam_items,
+                      "chunk_copies": tr.executor.stats.copies,
+                      "losses": [round(x, 6) for x in losses]}), flush=True)
 
 
 if __name__ == "__main__":
