@@ -74,7 +74,10 @@ def main():
     t0 = time.perf_counter()
     losses = []
     for i in range(a.steps):
-        loss = float(tr.step(batch()).item())
+        b = batch()
+        if i < 2 and os.environ.get("CS_DEMO_DEBUG"):
+            print("batch", i, int(b.sum()), int((b * torch.arange(b.numel(), device=b.device).view_as(b) % 1000003).sum()), flush=True)
+        loss = float(tr.step(b).item())
         losses.append(loss)
         if (i + 1) % a.every == 0 or i == 0:
             st = tr.step_state()
