@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--deterministic", action="store_true",
                     help="deterministic attention backend (bit-comparable runs)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--ckpt", action="store_true", help="activation checkpointing")
     a = ap.parse_args()
     import torch
     from paper_2108_05818_b200 import kernels as K
@@ -66,7 +68,9 @@ def main():
     hw = (HardwareSpec(gpu_count=1, gpu_bytes=int(a.gpu_gb * 1e9), cpu_bytes=150 * 10 ** 9)
           if a.gpu_gb else None)
     cap = 64 << 20 if a.hidden >= 2048 else 4 * a.hidden * a.hidden
-    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=cap, os_placement=a.os), hw, seed=0,
+    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=cap, os_placement=a.os,
+                                         checkpointing=a.ckpt), hw, seed=0,
+                      dtype=torch.bfloat16 if a.dtype == "bf16" else torch.float16,
                       hyper=K.AdamHyper(lr=a.lr, betas=(0.9, 0.95)), cuda_graph=not a.no_graph)
     if a.deterministic:
         from torch.nn.attention import SDPBackend, sdpa_kernel
