@@ -394,8 +394,9 @@ def test_cuda_graph_replay_with_checkpointing_and_bf16(ckpt, dtype):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
 
-@pytest.mark.parametrize("case", ["tiny_cap256Ki", "tiny_tight"])
-def test_overflow_steps_are_skipped_without_touching_the_model(case):
+@pytest.mark.parametrize("case,graph", [("tiny_cap256Ki", False), ("tiny_tight", False),
+                                        ("tiny_cap256Ki", True)])
+def test_overflow_steps_are_skipped_without_touching_the_model(case, graph):
     """Dynamic loss scaling from an absurd scale: the first steps overflow and
     are skipped.  A skipped step must leave the model exactly as it was —
     the fp16 chunks, which hold the step's gradients under the grad
@@ -405,11 +406,14 @@ def test_overflow_steps_are_skipped_without_touching_the_model(case):
     from paper_2108_05818_b200.trainer import ChunkTrainer
     c = CASES[case]
     schema = build_gpt_schema(**c["schema"])
+    kw = dict(cuda_graph=True, embedding_placement="gpu") if graph else {}
     tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
                       dtype=torch.float16, seed=0, init_loss_scale=2.0 ** 26,
-                      dynamic_loss_scale=True)
+                      dynamic_loss_scale=True, **kw)
     batch = _tokens(schema, 1)[0]
     losses = [tr.step_host(batch) for _ in range(16)]
+    if graph:  # captured while still overflowing: the skip decision is on the device
+        assert tr._graph is not None
     tr.finish_host_work()
     st = tr.step_state()
     skipped = 16 - int(st.step)
