@@ -72,16 +72,14 @@ def main():
                                          checkpointing=a.ckpt), hw, seed=0,
                       dtype=torch.bfloat16 if a.dtype == "bf16" else torch.float16,
                       hyper=K.AdamHyper(lr=a.lr, betas=(0.9, 0.95)), cuda_graph=not a.no_graph)
-    if a.deterministic:
+    if a.deterministic:  # keep the context object alive for the whole run
         from torch.nn.attention import SDPBackend, sdpa_kernel
-        sdpa_kernel(SDPBackend.MATH).__enter__()
+        deterministic_ctx = sdpa_kernel(SDPBackend.MATH)
+        deterministic_ctx.__enter__()
     t0 = time.perf_counter()
     losses = []
     for i in range(a.steps):
-        b = batch()
-        if i < 2 and os.environ.get("CS_DEMO_DEBUG"):
-            print("batch", i, int(b.sum()), int((b * torch.arange(b.numel(), device=b.device).view_as(b) % 1000003).sum()), flush=True)
-        loss = float(tr.step(b).item())
+        loss = float(tr.step(batch()).item())
         losses.append(loss)
         if (i + 1) % a.every == 0 or i == 0:
             st = tr.step_state()
