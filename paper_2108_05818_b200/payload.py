@@ -7,9 +7,11 @@ each decision real at the moment it is taken:
 reference accounting site             realisation here
 ====================================  =====================================================
 ``fetch_chunk`` / ``_evict_one``      ``copy``: cudaMemcpyAsync H2D/D2H of the whole chunk
-(`memory.py:207-221, 277-301`)        payload on a dedicated copy stream between pinned
-                                      host slabs and HBM; the compute stream waits on the
-                                      copy's event only when the chunk is next *used*
+(`memory.py:207-221, 277-301`)        payload on a copy stream per direction between pinned
+                                      host slabs and HBM slabs (:mod:`.slabs`); the compute
+                                      stream waits on the copy's event only when the chunk
+                                      is next *used*; fetches are prefetched from the
+                                      previous iteration's ledger
 ``place_payload`` / lazy OS birth     ``materialize``: an (uninitialised) payload born on
 (`memory.py:223-231`,                 the device; lazy optimizer state is initialised by
 `engine.py:234-240`)                  K6 ``cs_master_init`` reading the pinned fp32 init
@@ -23,13 +25,16 @@ reference accounting site             realisation here
 ``Engine._adam_event``                K2 grad sum-of-squares → device step scalars
 (`engine.py:225-272`)                 (clip / found-inf / loss scale) → ONE K1
                                       ``cs_adam_chunks`` launch over every GPU-placed local
-                                      position (+ the embedding); host K1 for CPU-placed ones
+                                      position (+ the non-chunked GPU parameters); host K1
+                                      for CPU-placed ones on a worker thread, whose
+                                      ``adam_copy`` H2D follows each update
 ====================================  =====================================================
 
 Chunk payloads are flat tensors of the chunk's full capacity (the reference
-charges full capacity, `chunks.py:99-102`).  HBM comes from PyTorch's caching
-allocator (chunk-sized blocks are recycled step to step), host slabs from
-its pinned caching host allocator.
+charges full capacity, `chunks.py:99-102`).  HBM payloads are slabs of the
+stream-ordered :class:`.slabs.SlabPool` (backed by PyTorch's caching
+allocator, compute-stream pool), host payloads come from its pinned caching
+host allocator.
 """
 
 import os
@@ -164,6 +169,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._plan = None
         self._host_state = None
         self._state_snap = None
+        self._keepalive: List[torch.Tensor] = []  # pinned inits K6 may still be reading
         #: run host Adam of CPU-placed positions on a worker thread, overlapping
         #: the main thread's enqueue of the rest of the step and the next
         #: forward (bit-identical).  12B with 58 host-placed positions: 2.05-2.62
@@ -686,7 +692,6 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         n = self.chunk_set.param_chunk(position).used_elems
         if device == GPU:
             K.master_init(p32, m, v, src, n)   # K6 reads the pinned fp32 init in place
-            self._keepalive = getattr(self, "_keepalive", [])
             self._keepalive.append(src)
         else:
             p32[:n].copy_(src[:n])
