@@ -64,7 +64,8 @@ def run_one(name: str) -> dict:
     tr = ChunkTrainer(schema, PolicySpec(capacity_elems=c["cap"], os_placement=c["os"],
                                          checkpointing=c.get("ckpt", False)),
                       hardware=hw, seed=0, hyper=K.AdamHyper(lr=1e-4), cuda_graph=True,
-                      embedding_placement=c.get("emb", "plan"), untied_head=c.get("untied"))
+                      embedding_placement=c.get("emb", "plan"), untied_head=c.get("untied"),
+                      prefetch_depth=int(os.environ.get("CS_PREFETCH_DEPTH", "2")))
     t_init = time.perf_counter() - t_init
     gen = torch.Generator().manual_seed(3)
     toks = [torch.randint(0, 50304, (c["batch"], 1025), generator=gen).cuda() for _ in range(2)]
@@ -117,7 +118,8 @@ def run_one(name: str) -> dict:
             "device_allocator": dev_alloc, "mem_get_info_end": [free_b, total_b],
             "slab_pool": {"allocs": tr.executor.slabs.allocs, "reuses": tr.executor.slabs.reuses,
                           "slab_bytes": tr.executor.slabs.slab_bytes},
-            "alloc_conf": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", ""), "pinned_alloc_during_timing": pinned,
+            "alloc_conf": os.environ.get("PYTORCH_CUDA_ALLOC_CONF", ""),
+            "prefetch_depth": tr.prefetch_depth, "pinned_alloc_during_timing": pinned,
             "pinned_stats_end": {k: v for k, v in hs1.items() if "current" in k or "peak" in k},
             "embedding_device": tr.embedding_placement,
             "host_embedding_s_per_step": (round(tr.host_embedding.host_seconds /
