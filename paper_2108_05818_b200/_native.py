@@ -120,6 +120,12 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    # torch first: it brings its own libcudart / libcublas / libcublasLt
+    # (same SONAMEs as the toolkit's).  Whichever copy is loaded first serves
+    # the whole process; if this library pulled the toolkit's libcublasLt in
+    # before torch, torch's libcublas would run against a libcublasLt of
+    # another version (CUBLAS_STATUS_INVALID_VALUE in its first GEMM).
+    import torch  # noqa: F401
     if not os.path.exists(LIB_PATH):
         raise NativeError("libchunkstar_b200.so not built (%s); run "
                           "`python -m paper_2108_05818_b200._build` — the chunk step "

@@ -49,3 +49,14 @@ def test_bench_two_ranks_gloo_same_device():
     cps = d["collectives_per_step"]
     assert cps["ledger_bytes_per_rank"] == cps["closed_form_bytes_per_rank"] > 0
     assert "collectives" in d
+
+
+def test_library_loaded_before_torch_keeps_torch_cublas_working():
+    """build() loads the library before any torch CUDA work (then smoke() runs
+    in the same process): torch's cuBLAS must still be the one in use."""
+    code = ("import __graft_entry__ as g; from paper_2108_05818_b200 import _native; "
+            "_native.load(); import torch; a = torch.randn(256, 256, device='cuda').half(); "
+            "print(float((a @ a).float().abs().sum()) > 0)")
+    res = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                         timeout=300)
+    assert res.returncode == 0 and res.stdout.strip().endswith("True"), res.stderr[-2000:]
