@@ -426,3 +426,27 @@ def test_overflow_steps_are_skipped_without_touching_the_model(case, graph):
         p16 = tr.local_chunk_payload(pos)[:n].cpu()
         p32 = tr.local_chunk_payload(pos, ChunkKind.PARAM_FP32)[:n].cpu()
         assert torch.equal(p16, p32.half())
+
+
+def test_gradient_clipping_in_the_real_step():
+    """max_grad_norm > 0: the device step scalars carry the global norm and
+    grad_scale = clip / loss_scale with clip = max_norm / norm (torch's
+    clip_grad_norm_ coefficient, eps 1e-6), and every K1 launch of the step
+    still matches the oracle bit for bit."""
+    from oracle import step_check
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_tight"]
+    schema = build_gpt_schema(**c["schema"])
+    tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                      dtype=torch.float16, seed=0, max_grad_norm=1e-3)
+    toks = _tokens(schema, 3)
+    tr.step_host(toks[0])
+    rec = step_check.arm(tr)
+    for t in toks[1:]:
+        assert np.isfinite(tr.step_host(t))
+    step_check.disarm(tr)
+    tr.finish_host_work()
+    st = tr.step_state()
+    assert st.grad_norm > 1e-3 and rec["checked"] > 0 and rec["mismatch"] == []
+    clip = 1e-3 / (st.grad_norm + 1e-6)
+    assert abs(st.grad_scale * st.loss_scale - clip) <= 1e-6 * clip
