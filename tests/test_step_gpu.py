@@ -450,3 +450,23 @@ def test_gradient_clipping_in_the_real_step():
     assert st.grad_norm > 1e-3 and rec["checked"] > 0 and rec["mismatch"] == []
     clip = 1e-3 / (st.grad_norm + 1e-6)
     assert abs(st.grad_scale * st.loss_scale - clip) <= 1e-6 * clip
+
+
+@pytest.mark.parametrize("place", ["cpu", "gpu"])
+def test_unfused_model_trains_like_fused(place):
+    """fused_ops=False (plain torch LayerNorm / GELU / embedding / loss, and
+    autograd gradients packed over the non-chunked parameters by K3 at ADAM)
+    through the same chunk-managed step: same ledgers as the fused model and
+    losses within fp16 tolerance."""
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_tight"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 4)
+    out = {}
+    for fused in (True, False):
+        tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                          dtype=torch.float16, seed=0, fused_ops=fused,
+                          embedding_placement=place, untied_head=True)
+        out[fused] = ([tr.step_host(t) for t in toks], [_ledger(r)["transfers"] for r in tr.reports])
+    assert out[True][1] == out[False][1]
+    np.testing.assert_allclose(out[True][0], out[False][0], rtol=2e-3)
