@@ -38,9 +38,9 @@ constexpr int kSumsqTile = kThreads * kGroups * 8;  // K2: 128-bit groups
 // every variant computes bit-identical results.
 struct AdamVariant { int groups, min_blocks; };
 constexpr AdamVariant kAdamVariants[] = {{4, 1}, {4, 4}, {2, 4}, {2, 6}, {8, 2}};
-constexpr int kAdamSimtVariants = 5;   // 5..17 = TMA-staged variants (adam_tma.cu)
-constexpr int kAdamVariantCount = 18;
-constexpr int kAdamDefault = 12;  // TMA-staged, 16 consumer warps, 4096 x 3 stages
+constexpr int kAdamSimtVariants = 5;   // 5..24 = TMA-staged variants (adam_tma.cu)
+constexpr int kAdamVariantCount = 25;
+constexpr int kAdamDefault = 21;  // TMA-staged, 20 consumer warps, 5120 x 3 stages
 
 struct AdamBatch {
   CsAdamItem item[cs::kMaxBatch];

@@ -480,6 +480,41 @@ int cs_adam_chunks_tma(const CsAdamItem* items, int n_items, int dtype, const Cs
       return cs_tma::launch<CS_FP16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
     return cs_tma::launch<CS_BF16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
   }
+  if (variant == 22) {  // 24 consumer warps, 5120 x 3 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 5120, 3, true, 24>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 5120, 3, true, 24>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 23) {  // 24 consumer warps, 4096 x 3 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 4096, 3, true, 24>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 4096, 3, true, 24>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 24) {  // 28 consumer warps, 5120 x 3 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 5120, 3, true, 28>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 5120, 3, true, 28>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 20) {  // 16 consumer warps, 5120 x 3 stages (215 KB of the 227 KB)
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 5120, 3, true, 16>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 5120, 3, true, 16>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 21) {  // 20 consumer warps, 5120 x 3 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 5120, 3, true, 20>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 5120, 3, true, 20>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 18) {  // 16 consumer warps, 3072 x 4 stages (two stages of loads in flight)
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 3072, 4, true, 16>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 3072, 4, true, 16>(items, n_items, h, d_state, s, 1);
+  }
+  if (variant == 19) {  // 16 consumer warps, 2560 x 5 stages
+    if (dtype == CS_FP16)
+      return cs_tma::launch<CS_FP16, 2560, 5, true, 16>(items, n_items, h, d_state, s, 1);
+    return cs_tma::launch<CS_BF16, 2560, 5, true, 16>(items, n_items, h, d_state, s, 1);
+  }
   if (variant == 16) {  // variant 12 with two 4-element groups per consumer pass
     if (dtype == CS_FP16)
       return cs_tma::launch<CS_FP16, 4096, 3, true, 16, 2>(items, n_items, h, d_state, s, 1);

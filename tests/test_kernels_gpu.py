@@ -34,7 +34,8 @@ def _oracle_state(O, st: "K.N.CsStepState"):
     return s
 
 
-@pytest.fixture(params=[0, 2, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17],
+@pytest.fixture(params=[0, 2, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23,
+                        24],
                 ids=lambda v: "variant%d" % v)
 def adam_variant(request, native_lib):
     old = native_lib.cs_adam_variant(-1)
