@@ -249,6 +249,11 @@ int cs_gemm_gelu(int mode, const void* w, const void* x, void* out, void* aux, i
                  int64_t O, int64_t K, int dtype, void* workspace, int64_t ws_bytes,
                  void* stream);
 
+/* Residual GEMM, out = x·Wᵀ + res with the residual read by the GEMM (C ≠ D,
+ * beta = 1): W [O,K], x [T,K], res / out [T,O] row-major; res is left intact. */
+int cs_gemm_res(const void* w, const void* x, const void* res, void* out, int64_t T, int64_t O,
+                int64_t K, int dtype, void* workspace, int64_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,17 +51,20 @@ int make_plan(int mode, int dtype, int64_t T, int64_t O, int64_t K, int64_t ws_b
               Plan* p) {
   const cudaDataType_t ty = dtype == CS_BF16 ? CUDA_R_16BF : CUDA_R_16F;
   LT(cublasLtMatmulDescCreate(&p->op, CUBLAS_COMPUTE_32F, CUDA_R_32F), "desc");
-  const cublasOperation_t ta = mode == 0 ? CUBLAS_OP_T : CUBLAS_OP_N;
+  const cublasOperation_t ta = mode == 1 ? CUBLAS_OP_N : CUBLAS_OP_T;
   const cublasOperation_t tb = CUBLAS_OP_N;
   LT(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta)), "transa");
   LT(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb)), "transb");
-  const cublasLtEpilogue_t epi = mode == 0 ? CUBLASLT_EPILOGUE_GELU_AUX : CUBLASLT_EPILOGUE_DGELU;
-  LT(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi)),
-     "epilogue");
-  const int64_t ld_aux = O;
-  LT(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_LD, &ld_aux,
-                                    sizeof(ld_aux)), "aux ld");
-  if (mode == 0) {  // A: W row-major [O,K] = column-major [K,O]
+  if (mode != 2) {
+    const cublasLtEpilogue_t epi =
+        mode == 0 ? CUBLASLT_EPILOGUE_GELU_AUX : CUBLASLT_EPILOGUE_DGELU;
+    LT(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi)),
+       "epilogue");
+    const int64_t ld_aux = O;
+    LT(cublasLtMatmulDescSetAttribute(p->op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_LD, &ld_aux,
+                                      sizeof(ld_aux)), "aux ld");
+  }
+  if (mode != 1) {  // A: W row-major [O,K] = column-major [K,O]
     LT(cublasLtMatrixLayoutCreate(&p->a, ty, K, O, K), "layout a");
   } else {          // A: W row-major [K,O] = column-major [O,K]
     LT(cublasLtMatrixLayoutCreate(&p->a, ty, O, K, O), "layout a");
@@ -119,4 +122,37 @@ extern "C" int cs_gemm_gelu(int mode, const void* w, const void* x, void* out, v
                     static_cast<cudaStream_t>(stream)), "matmul");
   return 0;  // a library (cuBLASLt) kernel: not counted in cs_launch_count
 
+}
+
+// Residual GEMM: out[T,O] = x[T,K] · W[O,K]ᵀ + res[T,O], with the residual read
+// by the GEMM itself (cuBLASLt C ≠ D, beta = 1).  torch.addmm(res, x, Wᵀ)
+// first copies res into its output and then accumulates (an extra 2·T·O·2
+// bytes per call); here the residual stream stays where it is (the
+// LayerNorm backward still needs it) and the sum lands in a new buffer.
+extern "C" int cs_gemm_res(const void* w, const void* x, const void* res, void* out, int64_t T,
+                           int64_t O, int64_t K, int dtype, void* workspace, int64_t ws_bytes,
+                           void* stream) {
+  if (!w || !x || !res || !out || T <= 0 || O <= 0 || K <= 0 ||
+      (dtype != CS_FP16 && dtype != CS_BF16) || ws_bytes < 0 || (ws_bytes > 0 && !workspace)) {
+    cs::set_error("cs_gemm_res: invalid argument");
+    return CS_EINVAL;
+  }
+  Plan* plan;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    if (!g_lt) LT(cublasLtCreate(&g_lt), "create");
+    const auto key = std::make_tuple(2, dtype, T, O, K, ws_bytes);
+    auto it = g_plans.find(key);
+    if (it == g_plans.end()) {
+      Plan p;
+      if (int e = make_plan(2, dtype, T, O, K, ws_bytes, &p)) return e;
+      it = g_plans.emplace(key, p).first;
+    }
+    plan = &it->second;
+  }
+  const float alpha = 1.0f, beta = 1.0f;
+  LT(cublasLtMatmul(g_lt, plan->op, &alpha, w, plan->a, x, plan->b, &beta, res, plan->d, out,
+                    plan->d, &plan->algo, workspace, (size_t)ws_bytes,
+                    static_cast<cudaStream_t>(stream)), "matmul");
+  return 0;
 }

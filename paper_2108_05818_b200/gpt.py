@@ -57,8 +57,18 @@ class _ChunkLinearFn(torch.autograd.Function):
         return dx, None, None
 
 
+def _residual_gemm(x2: torch.Tensor, w: torch.Tensor, r2: torch.Tensor) -> torch.Tensor:
+    """x Wᵀ + r with the residual read by the GEMM (cs_gemm_res) when the
+    operands are contiguous fp16/bf16 CUDA tensors, else torch.addmm."""
+    from . import kernels as K
+    if (x2.is_cuda and x2.dtype in K.DTYPE_CODE and x2.is_contiguous() and r2.is_contiguous()
+            and w.is_contiguous()):
+        return K.gemm_res(x2, w, r2)
+    return torch.addmm(r2, x2, w.t())
+
+
 class _ChunkLinearResFn(torch.autograd.Function):
-    """y = residual + x W^T with the add in the GEMM epilogue (beta = 1)."""
+    """y = residual + x W^T with the add inside the GEMM (C ≠ D, beta = 1)."""
 
     @staticmethod
     def forward(ctx, x: torch.Tensor, weight: nn.Parameter, residual: torch.Tensor,
@@ -67,7 +77,7 @@ class _ChunkLinearResFn(torch.autograd.Function):
         ctx.grad_sink = grad_sink
         ctx.save_for_backward(x)
         shp = residual.shape
-        out = torch.addmm(residual.reshape(-1, shp[-1]), x.reshape(-1, x.shape[-1]), weight.t())
+        out = _residual_gemm(x.reshape(-1, x.shape[-1]), weight, residual.reshape(-1, shp[-1]))
         return out.view(shp)
 
     @staticmethod
@@ -90,7 +100,7 @@ class _GeluLinearResFn(torch.autograd.Function):
         ctx.weight, ctx.grad_sink = weight, grad_sink
         ctx.save_for_backward(g, u)
         shp = residual.shape
-        out = torch.addmm(residual.reshape(-1, shp[-1]), g.reshape(-1, g.shape[-1]), weight.t())
+        out = _residual_gemm(g.reshape(-1, g.shape[-1]), weight, residual.reshape(-1, shp[-1]))
         return out.view(shp)
 
     @staticmethod

@@ -400,6 +400,25 @@ def gemm_dgelu(dy2d: torch.Tensor, w: torch.Tensor, u: torch.Tensor,
     return du
 
 
+def gemm_res(x2d: torch.Tensor, w: torch.Tensor, res2d: torch.Tensor,
+             stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """out = x·Wᵀ + res in one cuBLASLt GEMM that reads res itself (C ≠ D,
+    beta = 1) — torch.addmm would first copy res into its output."""
+    _need_cuda(x2d, w, res2d)
+    T, K_ = x2d.shape
+    O = w.shape[0]
+    if w.shape[1] != K_ or tuple(res2d.shape) != (T, O) or not x2d.is_contiguous() \
+            or not w.is_contiguous() or not res2d.is_contiguous():
+        raise ValueError("gemm_res: shapes/contiguity")
+    out = torch.empty(T, O, dtype=x2d.dtype, device=x2d.device)
+    ws = _lt_workspace(x2d.device)
+    N.check(N.load().cs_gemm_res(ctypes.c_void_p(w.data_ptr()), ctypes.c_void_p(x2d.data_ptr()),
+                                 ctypes.c_void_p(res2d.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                 T, O, K_, _code(x2d.dtype), ctypes.c_void_p(ws.data_ptr()),
+                                 ws.numel(), _stream(stream)), "cs_gemm_res")
+    return out
+
+
 def layernorm_supported(H: int) -> bool:
     return bool(N.load().cs_layernorm_supported(int(H)))
 

@@ -49,6 +49,15 @@ def main():
         print("  %8.1f  %s" % (g, n[:100]))
     small = [g for g, _ in gaps if g < 50]
     print("gaps < 50 us: %d totalling %.1f ms" % (len(small), sum(small) / 1e3))
+    agg = {}
+    for s_, e_, n in kern:
+        key = n[:60]
+        a = agg.setdefault(key, [0.0, 0])
+        a[0] += (e_ - s_) / 1e3
+        a[1] += 1
+    print("per-kernel time in these steps (ms, launches):")
+    for k, (t, c) in sorted(agg.items(), key=lambda x: -x[1][0])[:25]:
+        print("  %8.3f %5d  %s" % (t / 2, c // 2, k))
 
 
 if __name__ == "__main__":

@@ -412,3 +412,21 @@ def test_adam_chunks_8_byte_aligned_items_take_the_simt_path(native_lib, oracle_
     O.adam(rg, rp, rm, rv, n, O.FP16, 1e-3, 0.9, 0.999, 1e-8, 0.0, False, s)
     np.testing.assert_array_equal(dp.cpu().numpy().view(np.uint32), rp.view(np.uint32))
     np.testing.assert_array_equal(_bits16(d16), rg)
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_gemm_res_vs_torch_fp32(native_lib, dtype):
+    """cs_gemm_res: out = x·Wᵀ + res (residual read by the GEMM, res intact)
+    vs a plain PyTorch fp32 reference; tolerance a few 16-bit ulps of the
+    output scale."""
+    g = torch.Generator(device=DEV).manual_seed(3)
+    T, K_, O = 777, 512, 384
+    x = torch.randn(T, K_, device=DEV, generator=g).to(dtype)
+    w = (torch.randn(O, K_, device=DEV, generator=g) * 0.05).to(dtype)
+    r = torch.randn(T, O, device=DEV, generator=g).to(dtype)
+    r0 = r.clone()
+    out = K.gemm_res(x, w, r)
+    ref = x.float() @ w.float().t() + r.float()
+    tol = (2 ** -9 if dtype == torch.float16 else 2 ** -6) * ref.abs().max()
+    assert (out.float() - ref).abs().max() <= tol
+    assert torch.equal(r, r0)
