@@ -202,7 +202,8 @@ int cs_embed_fwd_host(const int64_t* tokens, int64_t n_tokens, int seq_len, cons
                       int n_threads);
 int cs_embed_bwd_host(const int64_t* tokens, int64_t n_tokens, int seq_len, const void* dout,
                       int64_t vocab, int hidden, void* gwte, void* gwpe, int dtype,
-                      int n_threads);
+                      int n_threads, double* sumsq /* nullable: sum of squares of the
+                      written gradients, double, row order (feeds the global norm) */);
 
 /* ---- device embedding operator (GPU-placed embedding) ----------------------------
  * The GPU branch of the same placement decision (`engine.py:214-219`), with the

@@ -80,7 +80,7 @@ SIGNATURES = {
     "cs_embed_bwd_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                          ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
-                                         ctypes.c_int]),
+                                         ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
     "cs_embed_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
                                     ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),

@@ -59,11 +59,31 @@ __attribute__((target("avx2,f16c"))) void fwd_rows(const int64_t* tok, int64_t n
   }
 }
 
+// Sum of squares of one stored (rounded) 16-bit row, in double, fixed order.
+template <int DT>
+__attribute__((target("avx2,f16c"))) double row_sumsq(const uint16_t* g, int H) {
+  __m256d acc0 = _mm256_setzero_pd(), acc1 = _mm256_setzero_pd();
+  for (int c = 0; c < H; c += 8) {
+    const __m256 f = load8<DT>(g + c);
+    const __m256d lo = _mm256_cvtps_pd(_mm256_castps256_ps128(f));
+    const __m256d hi = _mm256_cvtps_pd(_mm256_extractf128_ps(f, 1));
+    acc0 = _mm256_add_pd(acc0, _mm256_mul_pd(lo, lo));
+    acc1 = _mm256_add_pd(acc1, _mm256_mul_pd(hi, hi));
+  }
+  alignas(32) double t[8];
+  _mm256_store_pd(t, acc0);
+  _mm256_store_pd(t + 4, acc1);
+  return ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+}
+
 template <int DT>
 __attribute__((target("avx2,f16c"))) void bwd_rows(const int64_t* tok, int64_t n, int S,
                                                    const uint16_t* dout, int64_t V, int H,
                                                    uint16_t* gwte, uint16_t* gwpe,
-                                                   int threads) {
+                                                   int threads, double* sumsq) {
+  // per-row squared sums of the stored gradients (only rows a token hit are
+  // nonzero), reduced in row order below: deterministic for any thread count
+  std::vector<double> row_sq(sumsq ? V + S : 0, 0.0);
   // counting sort of token positions by row (stable: ascending i per row)
   std::vector<int64_t> start(V + 1, 0), order(n);
   for (int64_t i = 0; i < n; ++i) ++start[tok[i] + 1];
@@ -90,6 +110,7 @@ __attribute__((target("avx2,f16c"))) void bwd_rows(const int64_t* tok, int64_t n
           _mm256_storeu_ps(a + c, _mm256_add_ps(_mm256_loadu_ps(a + c), load8<DT>(d + c)));
       }
       for (int c = 0; c < H; c += 8) store8<DT>(g + c, _mm256_loadu_ps(a + c));
+      if (sumsq) row_sq[v] = row_sumsq<DT>(g, H);
     }
     const int64_t B = n / S;
 #pragma omp for schedule(static)
@@ -101,7 +122,13 @@ __attribute__((target("avx2,f16c"))) void bwd_rows(const int64_t* tok, int64_t n
           _mm256_storeu_ps(a + c, _mm256_add_ps(_mm256_loadu_ps(a + c), load8<DT>(d + c)));
       }
       for (int c = 0; c < H; c += 8) store8<DT>(gwpe + s * (int64_t)H + c, _mm256_loadu_ps(a + c));
+      if (sumsq) row_sq[V + s] = row_sumsq<DT>(gwpe + s * (int64_t)H, H);
     }
+  }
+  if (sumsq) {
+    double total = 0.0;
+    for (double x : row_sq) total += x;
+    *sumsq = total;
   }
 }
 
@@ -146,7 +173,7 @@ extern "C" int cs_embed_fwd_host(const int64_t* tokens, int64_t n_tokens, int se
 
 extern "C" int cs_embed_bwd_host(const int64_t* tokens, int64_t n_tokens, int seq_len,
                                  const void* dout, int64_t vocab, int hidden, void* gwte,
-                                 void* gwpe, int dtype, int n_threads) {
+                                 void* gwpe, int dtype, int n_threads, double* sumsq) {
   if (n_tokens < 0 || seq_len <= 0 || n_tokens % seq_len != 0 || vocab <= 0 || hidden <= 0 ||
       hidden % 8 != 0 || !gwte || !gwpe || (n_tokens > 0 && (!tokens || !dout)) ||
       (dtype != CS_FP16 && dtype != CS_BF16)) {
@@ -164,8 +191,8 @@ extern "C" int cs_embed_bwd_host(const int64_t* tokens, int64_t n_tokens, int se
   auto* gw = static_cast<uint16_t*>(gwte);
   auto* gp = static_cast<uint16_t*>(gwpe);
   if (dtype == CS_FP16)
-    bwd_rows<CS_FP16>(tokens, n_tokens, seq_len, d, vocab, hidden, gw, gp, threads);
+    bwd_rows<CS_FP16>(tokens, n_tokens, seq_len, d, vocab, hidden, gw, gp, threads, sumsq);
   else
-    bwd_rows<CS_BF16>(tokens, n_tokens, seq_len, d, vocab, hidden, gw, gp, threads);
+    bwd_rows<CS_BF16>(tokens, n_tokens, seq_len, d, vocab, hidden, gw, gp, threads, sumsq);
   return 0;
 }

@@ -50,6 +50,7 @@ class HostEmbedding:
         self._act_free: Optional[torch.cuda.Event] = None
         self.host_tokens: Optional[torch.Tensor] = None  # set by step_host (no D2H)
         self.grads_ready = False
+        self.grad_sumsq = 0.0      # of the last backward's gradients (cs_embed_bwd_host)
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.host_seconds = 0.0
@@ -128,7 +129,8 @@ class _HostEmbeddingFn(torch.autograd.Function):
         torch.cuda.current_stream(emb.device).synchronize()
         emb.d2h_bytes += dout.numel() * dout.element_size()
         t0 = time.perf_counter()
-        K.embed_bwd_host(tok, dout, emb.wte, emb.wpe, emb.threads)  # grad overwrite
+        # grad overwrite; the squares of the written rows come back with it
+        emb.grad_sumsq = K.embed_bwd_host(tok, dout, emb.wte, emb.wpe, emb.threads)
         emb.host_seconds += time.perf_counter() - t0
         emb.grads_ready = True
         return None, None, None

@@ -173,17 +173,20 @@ def embed_fwd_host(tokens: torch.Tensor, wte: torch.Tensor, wpe: torch.Tensor,
 
 
 def embed_bwd_host(tokens: torch.Tensor, dout: torch.Tensor, gwte: torch.Tensor,
-                   gwpe: torch.Tensor, n_threads: int = 0) -> None:
+                   gwpe: torch.Tensor, n_threads: int = 0) -> float:
     """Gradient of the lookup written over gwte [V, H] / gwpe [S, H]
-    (cs_embed_bwd_host; deterministic fp32 sums, ascending token order)."""
+    (cs_embed_bwd_host; deterministic fp32 sums, ascending token order).
+    Returns the sum of squares of the written gradients (double, row order)."""
     _host_contig(tokens, dout, gwte, gwpe)
     B, S = tokens.shape
     V, H = gwte.shape
     if gwpe.shape[0] != S:
         raise ValueError("gwpe must have seq_len rows")
+    out = ctypes.c_double(0.0)
     N.check(N.load().cs_embed_bwd_host(tokens.data_ptr(), B * S, S, dout.data_ptr(), V, H,
                                        gwte.data_ptr(), gwpe.data_ptr(), _code(gwte.dtype),
-                                       int(n_threads)), "cs_embed_bwd_host")
+                                       int(n_threads), ctypes.byref(out)), "cs_embed_bwd_host")
+    return out.value
 
 
 def embed_fwd(tokens: torch.Tensor, wte: torch.Tensor, wpe: torch.Tensor,

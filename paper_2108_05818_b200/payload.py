@@ -647,11 +647,16 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     d = g16.to(self.device, non_blocking=True)
                     self.comm.all_reduce_avg(d)
                     g16.copy_(d)
+        host_extra = 0.0
         if self.comm is None or self.comm.rank == 0:
             dev_items += emb_grads  # replicated after the all-reduce: count once
             if he is not None:
-                host_items += he.grad_items()
+                if self.comm is None or self.comm.world == 1:
+                    host_extra = he.grad_sumsq  # computed by the scatter, hit rows only
+                else:                           # averaged over ranks since: recount
+                    host_items += he.grad_items()
         host = K.grad_sumsq_host(host_items, self.host_threads) if host_items else 0.0
+        host += host_extra
         self.partials[-1:].fill_(host)
         K.grad_sumsq(dev_items, self.partials[:-1], dtype=self.dtype)
         K.sumsq_finalize(self.partials, self.state)

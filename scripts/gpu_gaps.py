@@ -17,11 +17,22 @@ def main():
     from paper_2108_05818_b200.config import PolicySpec
     from paper_2108_05818_b200.model import build_gpt_schema
     from paper_2108_05818_b200.trainer import ChunkTrainer
-    B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
-    schema = build_gpt_schema(layers=20, hidden_dim=2048, heads=16, seq_len=1024, vocab=50304,
-                              batch=B)
-    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=64 << 20), seed=0,
-                      hyper=K.AdamHyper(lr=1e-4))
+    arg = sys.argv[1] if len(sys.argv) > 1 else "32"
+    if arg.isdigit():
+        B = int(arg)
+        schema = build_gpt_schema(layers=20, hidden_dim=2048, heads=16, seq_len=1024,
+                                  vocab=50304, batch=B)
+        pol = PolicySpec(capacity_elems=64 << 20)
+    else:  # a scripts/configs_sweep.py configuration
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from configs_sweep import CONFIGS
+        c = CONFIGS[arg]
+        B = c["batch"]
+        schema = build_gpt_schema(layers=c["layers"], hidden_dim=c["hidden"], heads=c["heads"],
+                                  seq_len=1024, vocab=50304, batch=B)
+        pol = PolicySpec(capacity_elems=c["cap"], os_placement=c["os"],
+                         checkpointing=c.get("ckpt", False))
+    tr = ChunkTrainer(schema, pol, seed=0, hyper=K.AdamHyper(lr=1e-4))
     tok = torch.randint(0, 50304, (B, 1025)).cuda()
     for _ in range(3):
         tr.step(tok)

@@ -81,7 +81,7 @@ def test_argument_errors_of_model_side_entry_points(native_lib):
     assert lib.cs_embed_bwd(None, None, 5, 2, None, 10, 16, None, None, 0, N.CS_FP16,
                             None) == -1                                          # n % S
     assert lib.cs_embed_fwd_host(None, 1, 1, None, None, 10, 16, None, N.CS_FP16, 1) == -1
-    assert lib.cs_embed_bwd_host(None, 3, 2, None, 10, 16, None, None, N.CS_BF16, 1) == -1
+    assert lib.cs_embed_bwd_host(None, 3, 2, None, 10, 16, None, None, N.CS_BF16, 1, None) == -1
     assert lib.cs_layernorm_supported(2048) == 1 and lib.cs_layernorm_supported(100) == 0
     assert lib.cs_layernorm_fwd(None, None, None, None, 4, 100, 1e-5, N.CS_FP16, None) == -1
     assert lib.cs_xent_fwd(None, None, 4, 10, 7, None, None, None) != 0           # dtype

@@ -39,10 +39,18 @@ def test_embed_fwd_bwd_bit_exact(native_lib, oracle_lib, dtype, B, S, V, H, rep)
     assert np.array_equal(_bits(out), ref)
     gwte = torch.full((V, H), 7.0, dtype=dtype)   # overwritten, including unhit rows
     gwpe = torch.full((S, H), 7.0, dtype=dtype)
-    K.embed_bwd_host(tok, dout, gwte, gwpe, n_threads=3)
+    sq = K.embed_bwd_host(tok, dout, gwte, gwpe, n_threads=3)
     rw, rp = O.embed_bwd(tok.numpy(), _bits(dout), V, CODE[dtype])
     assert np.array_equal(_bits(gwte), rw)
     assert np.array_equal(_bits(gwpe), rp)
+    # the fused sum of squares = the squares of the written (rounded) gradients
+    ref_sq = sum(float((t.double() ** 2).sum()) for t in (gwte, gwpe))
+    assert sq == pytest.approx(ref_sq, rel=1e-12, abs=0.0)
+    assert sq == pytest.approx(K.grad_sumsq_host([(gwte.view(-1), V * H),
+                                                  (gwpe.view(-1), S * H)]), rel=1e-12)
+    # deterministic for any thread count (row-order reduction)
+    for threads in (1, 7):
+        assert K.embed_bwd_host(tok, dout, gwte.clone(), gwpe.clone(), n_threads=threads) == sq
 
 
 def test_oracle_forward_pinned_to_torch(oracle_lib):
