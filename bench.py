@@ -12,8 +12,9 @@ ZeRO chunk groups over NCCL (weak scaling: fixed per-GPU batch).
 
 Prints one JSON line (rank 0).  ``value`` = tokens/s over all ranks with
 inputs already in HBM (CUDA events, max over ranks); ``e2e`` = the same
-through ChunkTrainer.step_host (pinned host tokens H2D + loss D2H inside the
-timed region).  ``roofline`` = K1 fused chunk Adam timed in-region with
+through ChunkTrainer.step_host_async (pinned host tokens H2D + loss D2H of
+every step inside the timed region; step k's loss is read on the host once
+step k+1 is enqueued, the usual lagged loss logging).  ``roofline`` = K1 fused chunk Adam timed in-region with
 CUDA events on the compute stream.  ``cpu_baseline`` = the CPU port of the
 step (oracle/cpu_step.py) on a bounded sample, rank 0 at N=1 only.
 """
@@ -428,11 +429,23 @@ def main():
     # ---- timed region 2: end to end through the public API -----------------------
     torch.cuda.synchronize()
     barrier()
+    clocks2 = ClockSampler(local_rank)
+    clocks2.start()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0 = time.perf_counter()
-    for k in range(args.steps):
-        trainer.step_host(pool[k % 4])
+    d0.record()
+    pending = None
+    for k in range(args.steps):  # step k's loss is read once step k+1 is enqueued
+        nxt = trainer.step_host_async(pool[k % 4])
+        if pending is not None:
+            pending.result()
+        pending = nxt
+    pending.result()
+    d1.record()
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - e0) * 1e3 / args.steps
+    e2e_dev_ms = d0.elapsed_time(d1) / args.steps
+    clk2 = clocks2.stop()
     if world > 1:
         tt = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -476,7 +489,9 @@ def main():
                      "share_of_step": round(k1_avg_ms / ms, 4)},
         "e2e": {"value": round(tokens_per_step / (e2e_ms * 1e-3), 1), "unit": UNIT,
                 "h2d_bytes_per_step": pool[0].numel() * pool[0].element_size(),
-                "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_ms, 3)},
+                "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_ms, 3),
+                "device_ms_per_step": round(e2e_dev_ms, 3),
+                "sm_mhz": clk2.get("sm_mhz")},
         "gpu_launches": int(launches),
         "host_enqueue_ms_per_step": round(host_ms, 3),
         "cuda_graph": trainer._graph is not None,

@@ -44,6 +44,25 @@ def _host_ram_bytes() -> int:
         return 256 * 10**9
 
 
+class PendingLoss:
+    """A step's loss on its way to the host (pinned D2H + event)."""
+
+    __slots__ = ("_host", "_done")
+
+    def __init__(self, loss: torch.Tensor):
+        self._host = torch.empty((), dtype=loss.dtype, pin_memory=True)
+        self._host.copy_(loss, non_blocking=True)
+        self._done = torch.cuda.Event()
+        self._done.record()
+
+    def ready(self) -> bool:
+        return self._done.query()
+
+    def result(self) -> float:
+        self._done.synchronize()
+        return float(self._host)
+
+
 class ChunkTrainer:
     """Chunk-managed (PatrickStar) data-parallel GPT training on one GPU per rank."""
 
@@ -354,13 +373,24 @@ class ChunkTrainer:
 
     def step_host(self, tokens_host: torch.Tensor) -> float:
         """End-to-end step from host memory: H2D tokens, step, D2H loss."""
+        return self.step_host_async(tokens_host).result()
+
+    def step_host_async(self, tokens_host: torch.Tensor) -> "PendingLoss":
+        """`step_host` without waiting for the loss: H2D tokens (pinned host
+        memory; the caller keeps the buffer unchanged until the step has run),
+        enqueue the step, and a D2H of its loss into pinned memory whose
+        ``result()`` blocks only for that copy.  A training loop that reads
+        step k's loss after enqueueing step k+1 keeps the GPU busy across the
+        step boundary (the host's accounting and launch overlap the device)."""
         if self._graph is not None:  # land straight in the graph's input buffer
             self._static_tokens.copy_(tokens_host, non_blocking=True)
-            return float(self.step(self._static_tokens).item())
-        tokens = tokens_host.to(self.device, non_blocking=True)
-        if self.host_embedding is not None:  # the host lookup reads these, no D2H
-            self.host_embedding.host_tokens = tokens_host[:, :-1]
-        return float(self.step(tokens).item())
+            loss = self.step(self._static_tokens)
+        else:
+            tokens = tokens_host.to(self.device, non_blocking=True)
+            if self.host_embedding is not None:  # the host lookup reads these, no D2H
+                self.host_embedding.host_tokens = tokens_host[:, :-1]
+            loss = self.step(tokens)
+        return PendingLoss(loss)
 
     def finish_host_work(self) -> None:
         """Wait for the host-side work a step may leave running (the async

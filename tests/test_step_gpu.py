@@ -151,6 +151,40 @@ def test_cuda_graph_replay_matches_eager_steps():
         assert _ledger(r)["samples"] == ref["samples"]
 
 
+@pytest.mark.parametrize("case,graph", [("tiny_cap256Ki", True), ("tiny_tight", False)])
+def test_lagged_loss_reads_match_synchronous_steps(case, graph):
+    """step_host_async with step k's loss read after step k+1 is enqueued (the
+    bench's e2e loop) trains exactly like synchronous step_host: CUDA-graph
+    replay, and eager steps with evictions, host Adam and the CPU embedding."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES[case]
+    schema = build_gpt_schema(**c["schema"])
+    toks = [t.pin_memory() for t in _tokens(schema, 7)]
+    extra = dict(cuda_graph=True, embedding_placement="gpu") if graph else {}
+    out = []
+    with sdpa_kernel(SDPBackend.MATH):
+        for lagged in (False, True):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0, **extra)
+            if not lagged:
+                losses = [tr.step_host(t) for t in toks]
+            else:
+                pend = [tr.step_host_async(t) for t in toks[:1]]
+                for t in toks[1:]:
+                    pend.append(tr.step_host_async(t))
+                    pend[-2].result()
+                losses = [p.result() for p in pend]
+            tr.finish_host_work()
+            params = [tr.local_chunk_payload(p).cpu().clone()
+                      for p in range(tr.sim.chunk_set.positions)]
+            out.append((losses, params, tr._graph is not None))
+    assert out[0][2] == out[1][2] == graph
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1], out[1][1]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
 def test_checkpointing_does_not_change_numerics():
     """Recomputed activations give bit-identical training (deterministic attention)."""
     from torch.nn.attention import SDPBackend, sdpa_kernel
