@@ -12,7 +12,8 @@
  *  - plain C types only; device pointers are void* / float*, sizes int64_t;
  *  - every GPU entry point takes a cudaStream_t (passed as void*) and is
  *    asynchronous; the library never allocates, frees or synchronises
- *    device memory (the caller owns all buffers);
+ *    device memory (the caller owns all buffers) — except inside the NCCL
+ *    communicator that cs_comm_init creates;
  *  - return 0 on success, a cudaError_t (>0) from the launch, or a
  *    negative CS_E* argument error; cs_last_error() describes the last
  *    failure on the calling thread;
@@ -49,7 +50,8 @@ enum {
   CS_OK = 0,
   CS_EINVAL = -1,      /* bad argument (null pointer, negative count, dtype) */
   CS_EALIGN = -2,      /* a vectorised buffer is not 16-byte aligned */
-  CS_ETOOMANY = -3     /* work list longer than CS_MAX_ITEMS */
+  CS_ETOOMANY = -3,    /* work list longer than CS_MAX_ITEMS */
+  CS_EUNAVAIL = -4     /* NCCL could not be loaded (cs_comm_* / collectives) */
 };
 
 #define CS_MAX_ITEMS 4096
@@ -123,10 +125,12 @@ int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
                    void* stream);
 /* Tuning: select K1's data-movement variant (bit-identical results):
  * 0-4 SIMT register-tiled (groups/thread x min CTAs/SM), 5-7 TMA-staged
- * (cp.async.bulk + mbarrier ring; 5: 2048x4 stages, 6: 2048x3 at 2 CTAs/SM,
- * 7: 4096x3; 8-10 add a dedicated bulk-store warp: 2048x6, 2048x3 at
- * 2 CTAs/SM, 1024x4 at 3 CTAs/SM).  v < 0 only queries.  Default from
- * $CS_ADAM_VARIANT, else 0. */
+ * (cp.async.bulk + mbarrier ring), 8-24 TMA-staged with a dedicated
+ * bulk-store warp (tile size x stages x consumer warps; table in adam.cu,
+ * A/B results in profiles/r01/k1_variants.md).  v < 0 only queries.
+ * Default from $CS_ADAM_VARIANT, else 21 (5120-element tiles x 3 stages,
+ * 20 consumer warps).  Items whose pointers are not 16-byte aligned run on
+ * variant 0. */
 int cs_adam_variant(int v);
 
 /* ---- K2: gradient sum of squares -------------------------------------------
@@ -254,6 +258,27 @@ int cs_gemm_gelu(int mode, const void* w, const void* x, void* out, void* aux, i
  * beta = 1): W [O,K], x [T,K], res / out [T,O] row-major; res is left intact. */
 int cs_gemm_res(const void* w, const void* x, const void* res, void* out, int64_t T, int64_t O,
                 int64_t K, int dtype, void* workspace, int64_t ws_bytes, void* stream);
+
+/* ---- ZeRO chunk-group collectives (NCCL, loaded at first use) ---------------
+ * For callers without torch.distributed (the Python executor uses
+ * torch.distributed's NCCL by default; CS_COMM=native routes it here).
+ * Protocol of `/root/reference/pkg/src/chunkstar/parallel.py:196-264`:
+ * slot k of a p×count group buffer is rank k's chunk (position g·p+k,
+ * `parallel.py:107-114`).  Comm calls return ncclResult_t (>0) on an NCCL
+ * failure, CS_EUNAVAIL if libnccl.so.2 cannot be loaded.  Stream-ordered. */
+#define CS_COMM_ID_BYTES 128
+int cs_comm_version(void);                 /* NCCL_VERSION_CODE of the loaded NCCL */
+int cs_comm_unique_id(void* id_out);       /* rank 0; share the 128 bytes out of band */
+int cs_comm_init(const void* id, int nranks, int rank, void** comm);  /* current device */
+int cs_comm_destroy(void* comm);
+/* a18 (`parallel.py:196-223`): gather the group; in place when local is slot rank */
+int cs_allgather(void* group_buf, const void* local, int64_t count, int dtype, void* comm,
+                 void* stream);
+/* a20 (`parallel.py:241-264`): local = mean over ranks of slot rank of group_buf */
+int cs_reduce_scatter_avg(void* local, const void* group_buf, int64_t count, int dtype,
+                          void* comm, void* stream);
+/* replicated (non-chunked) grads: avg=1; the global sum of squares: avg=0, CS_FP32 */
+int cs_allreduce(void* buf, int64_t count, int dtype, int avg, void* comm, void* stream);
 
 #ifdef __cplusplus
 }

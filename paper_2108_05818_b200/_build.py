@@ -20,7 +20,7 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libchunkstar_b200.so")
 
 CUDA_SOURCES = ["adam.cu", "adam_tma.cu", "pack.cu", "xent.cu", "layernorm.cu", "embed.cu"]
-HOST_SOURCES = ["host_adam.cpp", "host_embed.cpp", "capi.cpp", "gemm_gelu.cpp"]
+HOST_SOURCES = ["host_adam.cpp", "host_embed.cpp", "capi.cpp", "gemm_gelu.cpp", "comm.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 ORACLE_DIR = os.path.join(ROOT, "oracle")
@@ -78,7 +78,7 @@ def build_library(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
     tmp = LIB + ".tmp"
     _run([_nvcc(), *ARCH, "-shared", "-cudart", "shared", "-o", tmp, *objs,
-          "-Xcompiler", "-fopenmp", "-lgomp", "-lcublasLt"], verbose)
+          "-Xcompiler", "-fopenmp", "-lgomp", "-lcublasLt", "-ldl"], verbose)
     os.replace(tmp, LIB)
     return LIB
 

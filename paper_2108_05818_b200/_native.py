@@ -110,6 +110,17 @@ SIGNATURES = {
     "cs_xent_bwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.c_float, ctypes.c_int64,
                                    ctypes.c_int64, ctypes.c_int, ctypes.c_void_p]),
+    "cs_comm_version": (ctypes.c_int, []),
+    "cs_comm_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
+    "cs_comm_init": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_void_p)]),
+    "cs_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "cs_allgather": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "cs_reduce_scatter_avg": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                             ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
+    "cs_allreduce": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_void_p, ctypes.c_void_p]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

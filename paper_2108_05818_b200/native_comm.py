@@ -1,0 +1,127 @@
+"""Chunk-group collectives through the library's C ABI (``cs_comm_*``,
+``cs_allgather``, ``cs_reduce_scatter_avg``, ``cs_allreduce``).
+
+Same interface and semantics as :class:`.payload.ChunkComm` (the
+reference's protocol, `parallel.py:196-264`), but the NCCL communicator is the
+library's own, so a non-Python host (the cgo / JNI bindings in INTEGRATION.md)
+drives exactly the calls the Python executor makes.  ``ChunkTrainer`` uses it
+when ``CS_COMM=native``; the default is torch.distributed's NCCL.
+torch.distributed is used only to broadcast the 128-byte unique id.
+
+Async ops run on a dedicated comm stream that first waits for the caller's
+stream; the returned work's ``wait()`` orders the caller's current stream
+after the collective (no host wait), like torch's NCCL work objects.
+"""
+
+import ctypes
+from typing import List, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+CODE = {torch.float16: N.CS_FP16, torch.bfloat16: N.CS_BF16, torch.float32: N.CS_FP32}
+
+
+class _Work:
+    __slots__ = ("_event",)
+
+    def __init__(self, event: torch.cuda.Event):
+        self._event = event
+
+    def wait(self) -> None:
+        torch.cuda.current_stream().wait_event(self._event)
+
+    def is_completed(self) -> bool:
+        return self._event.query()
+
+
+class NativeChunkComm:
+    """One rank's library-owned NCCL communicator over a process group."""
+
+    def __init__(self, group: Optional["dist.ProcessGroup"] = None,
+                 device: Optional[torch.device] = None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
+        self.calls: List[Tuple[str, int]] = []
+        lib = N.load()
+        uid = b"\0" * 128
+        if self.rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            N.check(lib.cs_comm_unique_id(buf), "cs_comm_unique_id")
+            uid = buf.raw
+        box = [uid]
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(box, src=src, group=group)
+        self._comm = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            N.check(lib.cs_comm_init(box[0], self.world, self.rank, ctypes.byref(self._comm)),
+                    "cs_comm_init")
+        self.stream = torch.cuda.Stream(self.device)
+
+    def close(self) -> None:
+        if self._comm:
+            N.check(N.load().cs_comm_destroy(self._comm), "cs_comm_destroy")
+            self._comm = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _run(self, call, async_op: bool, *tensors: torch.Tensor):
+        cur = torch.cuda.current_stream(self.device)
+        self.stream.wait_stream(cur)
+        for t in tensors:  # the caching allocator must not recycle them under the op
+            t.record_stream(self.stream)
+        call(ctypes.c_void_p(self.stream.cuda_stream))
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        work = _Work(ev)
+        if async_op:
+            return work
+        work.wait()
+        return None
+
+    @staticmethod
+    def _code(t: torch.Tensor) -> int:
+        if t.dtype not in CODE or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("native collectives take contiguous CUDA fp16/bf16/fp32 tensors")
+        return CODE[t.dtype]
+
+    def all_gather_slab(self, slab: torch.Tensor, async_op: bool = False):
+        """In place: slot ``rank`` of ``slab`` is this rank's contribution."""
+        cap = slab.numel() // self.world
+        code = self._code(slab)
+        mine = slab.data_ptr() + self.rank * cap * slab.element_size()
+        self.calls.append(("all_gather", slab.numel() * slab.element_size()))
+        lib = N.load()
+        return self._run(lambda s: N.check(lib.cs_allgather(slab.data_ptr(), mine, cap, code,
+                                                            self._comm, s), "cs_allgather"),
+                         async_op, slab)
+
+    def reduce_scatter_avg(self, out: torch.Tensor, slab: torch.Tensor, async_op: bool = False):
+        code = self._code(slab)
+        if out.numel() * self.world != slab.numel() or out.dtype != slab.dtype:
+            raise ValueError("reduce_scatter_avg: out must be one slot of the group buffer")
+        self.calls.append(("reduce_scatter", slab.numel() * slab.element_size()))
+        lib = N.load()
+        return self._run(lambda s: N.check(lib.cs_reduce_scatter_avg(
+            out.data_ptr(), slab.data_ptr(), out.numel(), code, self._comm, s),
+            "cs_reduce_scatter_avg"), async_op, out, slab)
+
+    def _all_reduce(self, t: torch.Tensor, avg: int) -> None:
+        code = self._code(t)
+        lib = N.load()
+        self._run(lambda s: N.check(lib.cs_allreduce(t.data_ptr(), t.numel(), code, avg,
+                                                     self._comm, s), "cs_allreduce"), False, t)
+
+    def all_reduce_sum(self, t: torch.Tensor) -> None:
+        self._all_reduce(t, 0)
+
+    def all_reduce_avg(self, t: torch.Tensor) -> None:
+        self._all_reduce(t, 1)

@@ -91,7 +91,11 @@ class ChunkTrainer:
         nproc, rank = 1, 0
         if process_group is not None or (torch.distributed.is_initialized()
                                          and torch.distributed.get_world_size() > 1):
-            comm = ChunkComm(process_group)
+            if os.environ.get("CS_COMM", "torch") == "native":  # the C-ABI communicator
+                from .native_comm import NativeChunkComm
+                comm = NativeChunkComm(process_group, self.device)
+            else:
+                comm = ChunkComm(process_group)
             nproc, rank = comm.world, comm.rank
         if hardware is None:
             total = torch.cuda.get_device_properties(self.device).total_memory

@@ -82,6 +82,13 @@ def test_argument_errors_of_model_side_entry_points(native_lib):
                             None) == -1                                          # n % S
     assert lib.cs_embed_fwd_host(None, 1, 1, None, None, 10, 16, None, N.CS_FP16, 1) == -1
     assert lib.cs_embed_bwd_host(None, 3, 2, None, 10, 16, None, None, N.CS_BF16, 1, None) == -1
+    # collectives: arguments are checked before NCCL is even loaded
+    assert lib.cs_allgather(None, None, 4, N.CS_FP16, None, None) == -1
+    assert lib.cs_reduce_scatter_avg(None, None, 4, N.CS_BF16, None, None) == -1
+    assert lib.cs_allreduce(None, 1, N.CS_FP32, 0, None, None) == -1
+    assert lib.cs_comm_init(b"\0" * 128, 2, 2, None) == -1                        # rank >= n
+    assert lib.cs_comm_unique_id(None) == -1
+    assert lib.cs_comm_destroy(None) == 0
     assert lib.cs_layernorm_supported(2048) == 1 and lib.cs_layernorm_supported(100) == 0
     assert lib.cs_layernorm_fwd(None, None, None, None, 4, 100, 1e-5, N.CS_FP16, None) == -1
     assert lib.cs_xent_fwd(None, None, 4, 10, 7, None, None, None) != 0           # dtype
