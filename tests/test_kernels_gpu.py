@@ -430,3 +430,52 @@ def test_gemm_res_vs_torch_fp32(native_lib, dtype):
     tol = (2 ** -9 if dtype == torch.float16 else 2 ** -6) * ref.abs().max()
     assert (out.float() - ref).abs().max() <= tol
     assert torch.equal(r, r0)
+
+
+def test_k1_at_the_bench_layout_every_element_bit_exact(native_lib, oracle_lib):
+    """K1 at BASELINE's full size: the 1B bench model's 15 chunk positions
+    (cap 64Mi, 1,006,632,960 used elements, the chunk layout of
+    `chunks.py:168-201`) in ONE default-variant launch, every element of p16,
+    p32, m and v compared with the C oracle (slice by slice on the host)."""
+    from paper_2108_05818_b200.chunks import build_model_chunk_lists
+    from paper_2108_05818_b200.model import build_gpt_schema
+    O = oracle_lib
+    cap = 64 << 20
+    schema = build_gpt_schema(layers=20, hidden_dim=2048, heads=16, seq_len=1024,
+                              vocab=50304, batch=32)
+    cs = build_model_chunk_lists(schema, cap)
+    used = [cs.param_chunk(p).used_elems for p in range(cs.positions)]
+    assert len(used) == 15 and sum(used) == 1_006_632_960
+    g = torch.Generator(device=DEV).manual_seed(11)
+    items, host = [], []
+    for n in used:
+        p16 = (torch.randn(cap, device=DEV, generator=g) * 1e-2).half()
+        p32 = torch.randn(cap, device=DEV, generator=g) * 0.02
+        m = torch.randn(cap, device=DEV, generator=g) * 1e-3
+        v = torch.rand(cap, device=DEV, generator=g) * 1e-5
+        items.append((p16, p32, m, v, n))
+    hyper = K.AdamHyper(lr=1e-4)
+    state = K.StepState(DEV)
+    state.sumsq().fill_(4.0)
+    K.adam_prepare(state, hyper)
+    s = _oracle_state(O, state.read())
+    # inputs to the host in 8Mi slices (bounded host memory per slice pair)
+    sl = 8 << 20
+    for p16, p32, m, v, n in items:
+        host.append([(_bits16(p16[a:min(a + sl, n)]), p32[a:a + sl][:n - a].cpu().numpy(),
+                      m[a:a + sl][:n - a].cpu().numpy(), v[a:a + sl][:n - a].cpu().numpy())
+                     for a in range(0, n, sl)])
+    tail = [(it[0][it[4]:].clone(), it[1][it[4]:].clone()) for it in items]
+    K.adam_chunks(items, hyper, state)
+    torch.cuda.synchronize()
+    for (p16, p32, m, v, n), slices, (t16, t32) in zip(items, host, tail):
+        for k, (rg, rp, rm, rv) in enumerate(slices):
+            a = k * sl
+            b = a + rg.size
+            O.adam(rg, rp, rm, rv, b - a, O.FP16, 1e-4, 0.9, 0.999, 1e-8, 0.0, False, s)
+            assert np.array_equal(_bits16(p16[a:b]), rg)
+            assert np.array_equal(p32[a:b].cpu().numpy().view(np.uint32), rp.view(np.uint32))
+            assert np.array_equal(m[a:b].cpu().numpy().view(np.uint32), rm.view(np.uint32))
+            assert np.array_equal(v[a:b].cpu().numpy().view(np.uint32), rv.view(np.uint32))
+        # the unused tail of each chunk is never touched
+        assert torch.equal(p16[n:], t16) and torch.equal(p32[n:], t32)
