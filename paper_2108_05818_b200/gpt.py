@@ -31,7 +31,7 @@ reuse of PatrickStar §4 with zero extra traffic (the K3 pack kernel is used
 where a gradient arrives from autograd instead, e.g. the embedding).
 """
 
-from typing import Callable, List, Optional, Sequence, Tuple
+from typing import Callable, List, Optional, Tuple
 
 import torch
 import torch.nn as nn

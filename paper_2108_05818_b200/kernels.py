@@ -8,7 +8,7 @@ no CPU path for GPU-resident work.
 """
 
 import ctypes
-from typing import Iterable, List, Optional, Sequence, Tuple
+from typing import Optional, Sequence, Tuple
 
 import torch
 

@@ -21,7 +21,7 @@ records the access trace; the placement plan is computed at its ADAM event
 
 import os
 import time
-from typing import Callable, List, Optional, Tuple
+from typing import Callable, List, Optional
 
 import torch
 

@@ -14,7 +14,6 @@ import os
 import pytest
 
 from paper_2108_05818_b200.config import HardwareSpec, PolicySpec
-from paper_2108_05818_b200.memory import EvictionStrategy
 from paper_2108_05818_b200.model import build_gpt_schema
 from paper_2108_05818_b200.scenario import Simulator
 
