@@ -94,10 +94,28 @@ __device__ __forceinline__ uint16_t from_f(float f) {
 
 struct Consts {
   float gs, nss, sb, b2, c1, c2, eps, wd, decay;
+  double rsb;  // RN_f64(1 / sb), for div_by_sb
   bool adamw;
 };
 
-// identical op sequence to adam.cu's adam1 (torch.optim.Adam association)
+// x / sb rounded to float, bit-identical to __fdiv_rn(x, sb), in three
+// instructions instead of the IEEE division sequence (MUFU.RCP, FCHK, Newton
+// FFMAs and the slow-path branch).  Why exact: q = RN_f64(x * RN_f64(1/sb)) is
+// within ~2^-52 relative of x/sb.  Rounding q to float gives RN_f32(x/sb)
+// unless x/sb lies within 2^-52 relative of a float rounding midpoint M.
+// x/sb is never exactly on M: M has a 25-bit odd significand, so sb * M needs
+// more than 24 bits and cannot equal the float x.  Nor can it be closer to M
+// than 2^-49 relative: x - sb*M is a nonzero multiple of ulp(sb)*ulp(M)/2.
+// The quotient here is sqrt(v)/sqrt(1 - beta2^t): zero, a normal float, or
+// inf/nan, which pass through the conversions unchanged.  No subnormal or
+// overflowing results: sqrt(v) >= 2^-75 for v > 0, and sb lies in
+// [sqrt(1 - beta2), 1].  tests/test_kernels_gpu.py checks every variant
+// against the oracle's IEEE division, at the full bench size too.
+__device__ __forceinline__ float div_by_sb(float x, const Consts& c) {
+  return __double2float_rn(__dmul_rn((double)x, c.rsb));
+}
+
+// same op sequence and rounding as adam.cu's adam1 (torch.optim.Adam association)
 __device__ __forceinline__ void adam1(float g16, float& p, float& m, float& v, const Consts& c) {
   float g = __fmul_rn(g16, c.gs);
   if (c.wd != 0.0f) {
@@ -106,7 +124,7 @@ __device__ __forceinline__ void adam1(float g16, float& p, float& m, float& v, c
   }
   m = __fmaf_rn(c.c1, __fsub_rn(g, m), m);
   v = __fmaf_rn(__fmul_rn(c.c2, g), g, __fmul_rn(v, c.b2));
-  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.sb), c.eps);
+  const float denom = __fadd_rn(div_by_sb(__fsqrt_rn(v), c), c.eps);
   p = __fadd_rn(p, __fdiv_rn(__fmul_rn(c.nss, m), denom));
 }
 
@@ -175,6 +193,7 @@ adam_tma_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict__
   c.gs = st->grad_scale;
   c.nss = -st->step_size;
   c.sb = st->sqrt_bc2;
+  c.rsb = __ddiv_rn(1.0, (double)c.sb);
   c.b2 = b.b2;
   c.c1 = b.c1;
   c.c2 = b.c2;
@@ -321,6 +340,7 @@ adam_tma3_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict_
   c.gs = st->grad_scale;
   c.nss = -st->step_size;
   c.sb = st->sqrt_bc2;
+  c.rsb = __ddiv_rn(1.0, (double)c.sb);
   c.b2 = b.b2;
   c.c1 = b.c1;
   c.c2 = b.c2;
