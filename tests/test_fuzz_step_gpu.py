@@ -2,7 +2,8 @@
 
 Beyond the 13 golden configurations: for each seed a random tiny GPT (layers,
 hidden, sequence, batch), chunk capacity, dtype, eviction strategy, optimizer
-state placement, activation checkpointing and a GPU budget just above the
+state placement, activation checkpointing, Adam / AdamW hyper-parameters
+(learning rate, weight decay) and a GPU budget just above the
 smallest feasible one (found with the accounting-only engine, so the run
 evicts).  Properties checked on every configuration:
 
@@ -11,6 +12,8 @@ evicts).  Properties checked on every configuration:
   configuration (the accounting core is pinned to the reference by
   tests/test_decisions_golden.py);
 * the executor moved exactly the billed chunk bytes;
+* every K1 launch of the tight-budget run equals the C oracle byte for byte
+  (random lr, betas, weight decay, Adam / AdamW);
 * numerics: the tight-budget run — with a random embedding placement
   (plan / host / device operator) and synchronous or asynchronous host Adam —
   is bit-identical to an all-resident run of the same model (deterministic
@@ -47,7 +50,10 @@ def _config(seed):
     dtype = r.choice([torch.float16, torch.bfloat16])
     run = dict(embedding_placement=r.choice(["plan", "cpu", "gpu"]),
                async_host_adam=r.random() < 0.5)
-    return schema, policy, dtype, r.uniform(1.05, 1.4), run
+    wd = r.choice([0.0, 0.0, 0.01, 0.1])
+    hyper = dict(lr=r.choice([1e-4, 1e-3]), betas=r.choice([(0.9, 0.999), (0.9, 0.95)]),
+                 weight_decay=wd, adamw=wd > 0 and r.random() < 0.5)
+    return schema, policy, dtype, r.uniform(1.05, 1.4), run, hyper
 
 
 def _feasible(schema, policy, gpu_bytes):
@@ -80,7 +86,8 @@ def _rows(r):
 def test_random_config_real_step(seed):
     from torch.nn.attention import SDPBackend, sdpa_kernel
     from paper_2108_05818_b200.trainer import ChunkTrainer
-    schema_kw, policy, dtype, slack, knobs = _config(seed)
+    from paper_2108_05818_b200 import kernels as K
+    schema_kw, policy, dtype, slack, knobs, hyper = _config(seed)
     budget = _tight_budget(schema_kw, policy, slack)
     ok, ref = _feasible(schema_kw, policy, budget)
     assert ok
@@ -94,9 +101,15 @@ def test_random_config_real_step(seed):
             kw = knobs if name == "tight" else {}
             tr = ChunkTrainer(schema, PolicySpec(**policy),
                               HardwareSpec(gpu_count=1, gpu_bytes=gpu_bytes), dtype=dtype, seed=0,
-                              untied_head=True, **kw)
+                              untied_head=True, hyper=K.AdamHyper(**hyper), **kw)
+            if name == "tight":  # every K1 launch of the tight run replayed by the C oracle
+                from oracle import step_check
+                rec = step_check.arm(tr)
             losses = [tr.step_host(t) for t in toks]
             tr.finish_host_work()
+            if name == "tight":
+                step_check.disarm(tr)
+                assert rec["mismatch"] == [], (seed, rec["mismatch"][:3])
             params = [tr.local_chunk_payload(p).cpu().clone()
                       for p in range(tr.sim.chunk_set.positions)]
             out[name] = (losses, params, tr)
