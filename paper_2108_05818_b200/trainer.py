@@ -79,7 +79,8 @@ class ChunkTrainer:
                  prefetch_depth: int = 2, non_model: str = "analytic",
                  gather_depth: int = 2, embedding_placement: str = "plan",
                  untied_head: Optional[bool] = None,
-                 async_host_adam: Optional[bool] = None):
+                 async_host_adam: Optional[bool] = None,
+                 comm=None):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -87,10 +88,11 @@ class ChunkTrainer:
         self.schema = schema
         self.dtype = dtype
         self.policy = policy or PolicySpec()
-        comm = None
         nproc, rank = 1, 0
-        if process_group is not None or (torch.distributed.is_initialized()
-                                         and torch.distributed.get_world_size() > 1):
+        if comm is not None:  # a caller-supplied communicator with ChunkComm's interface
+            nproc, rank = comm.world, comm.rank
+        elif process_group is not None or (torch.distributed.is_initialized()
+                                           and torch.distributed.get_world_size() > 1):
             if os.environ.get("CS_COMM", "torch") == "native":  # the C-ABI communicator
                 from .native_comm import NativeChunkComm
                 comm = NativeChunkComm(process_group, self.device)
