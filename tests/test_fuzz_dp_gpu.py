@@ -6,7 +6,9 @@ every rank (found with the accounting-only engine, so gathered remote chunks
 get evicted).  Every rank's transfer and collective ledgers must equal the
 accounting-only engine of that rank (pinned to the reference on random
 configurations by tests/test_decisions_fuzz.py), and every rank must move
-exactly the bytes it bills."""
+exactly the bytes it bills.  Odd seeds run with collectives that land late on a
+side stream with NaN-poisoned receive buffers (tests/test_dp_stream_order_gpu.py),
+so every read of collective results must be stream-ordered as under NCCL."""
 
 import os
 import random
@@ -62,7 +64,7 @@ def _rows(r):
              for c in r.collectives])
 
 
-def _worker(rank, world, port, outdir, schema_kw, policy, budget):
+def _worker(rank, world, port, outdir, schema_kw, policy, budget, late=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -73,15 +75,19 @@ def _worker(rank, world, port, outdir, schema_kw, policy, budget):
         from paper_2108_05818_b200.trainer import ChunkTrainer
         schema = build_gpt_schema(**schema_kw)
         pol = PolicySpec(**dict(policy, eviction=EvictionStrategy(policy["eviction"])))
+        comm = None
+        if late:  # collectives that land late on a side stream (NCCL-style completion)
+            from test_dp_stream_order_gpu import StreamOrderedComm
+            comm = StreamOrderedComm()
         tr = ChunkTrainer(schema, pol, HardwareSpec(gpu_count=world, gpu_bytes=budget),
-                          dtype=torch.float16, seed=0)
+                          dtype=torch.float16, seed=0, comm=comm)
         g = torch.Generator().manual_seed(rank)
-        for _ in range(ITERS):
-            tr.step_host(torch.randint(0, schema.vocab, (schema.batch, schema.seq_len + 1),
-                                       generator=g))
+        losses = [tr.step_host(torch.randint(0, schema.vocab, (schema.batch, schema.seq_len + 1),
+                                             generator=g)) for _ in range(ITERS)]
         tr.finish_host_work()
         st = tr.executor.stats
-        torch.save({"rows": [_rows(r) for r in tr.reports],
+        torch.save({"rows": [_rows(r) for r in tr.reports], "losses": losses,
+                    "applied": int(tr.step_state().step),
                     "h2d": st.h2d_bytes - st.prefetch_discarded_bytes, "d2h": st.d2h_bytes},
                    os.path.join(outdir, "rank%d.pt" % rank))
     finally:
@@ -94,12 +100,14 @@ def test_random_config_real_zero_step(seed):
     budget = _budget(schema, policy, world, slack)
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(world, 29300 + seed * 10 + os.getpid() % 50 * 50, d, schema,
-                                policy, budget), nprocs=world, join=True)
+                                policy, budget, seed % 2 == 1), nprocs=world, join=True)
         res = [torch.load(os.path.join(d, "rank%d.pt" % k), weights_only=False)
                for k in range(world)]
     for k in range(world):
         ref = _sim(schema, policy, world, k, budget)
         assert res[k]["rows"] == [_rows(r) for r in ref.reports], (seed, k)
+        assert all(x == x and abs(x) < 1e4 for x in res[k]["losses"]) and \
+            res[k]["applied"] == ITERS, (seed, k, res[k]["losses"])
         billed = [t for r in ref.reports for t in r.transfers if t.chunk_id != "embedding"]
         assert res[k]["h2d"] == sum(t.bytes for t in billed if (t.src, t.dst) == ("cpu", "gpu"))
         assert res[k]["d2h"] == sum(t.bytes for t in billed if (t.src, t.dst) == ("gpu", "cpu"))
