@@ -142,6 +142,10 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.comm = comm
         self.host_threads = host_threads
         self.time_copies = time_copies
+        # test knob: every chunk move first spins this many cycles on its copy
+        # stream, and an H2D destination reads NaN until the bytes land, so a
+        # consumer not ordered after the move's event sees garbage
+        self.copy_delay_cycles = 0
         self._setup_device(init_loss_scale)
         self.payload: Dict[str, Dict[int, torch.Tensor]] = {GPU: {}, CPU: {}}
         self.ready: Dict[Tuple[int, str], torch.cuda.Event] = {}
@@ -385,6 +389,10 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             t0 = torch.cuda.Event(enable_timing=True) if self.time_copies else None
             if t0 is not None:
                 t0.record(cs)
+            if self.copy_delay_cycles:
+                if dst == GPU:
+                    d.fill_(float("nan"))
+                torch.cuda._sleep(self.copy_delay_cycles)
             d.copy_(s, non_blocking=True)
             done = torch.cuda.Event(enable_timing=self.time_copies)
             done.record(cs)

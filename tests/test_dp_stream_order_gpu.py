@@ -9,7 +9,8 @@ result LATE: on a side stream, after a ~1 ms spin, with the receive buffer
 poisoned (NaN) in the meantime.  A gather slot read before its ``wait()``, a
 reduce-scatter output consumed early, or a group slab recycled while the
 collective still writes it turns into NaN losses, skipped steps or a ledger /
-loss mismatch.  Cases follow tests/test_dp_step_gpu.py.
+loss mismatch.  Chunk moves are delayed the same way (the executor's
+``copy_delay_cycles`` knob).  Cases follow tests/test_dp_step_gpu.py.
 """
 
 import gzip
@@ -119,6 +120,7 @@ def _worker(rank, world, port, outdir, case, place, async_adam):
                           untied_head=True if place != "plan" else None,
                           async_host_adam=async_adam, comm=comm)
         assert tr.nproc == world and tr.rank == rank and tr.executor.comm is comm
+        tr.executor.copy_delay_cycles = 1_000_000  # chunk moves land late as well
         losses = [tr.step_host(b) for b in _batches(schema, rank, ITERS)]
         tr.finish_host_work()
         torch.cuda.synchronize()
