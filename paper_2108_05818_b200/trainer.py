@@ -19,6 +19,7 @@ records the access trace; the placement plan is computed at its ADAM event
 (`engine.py:282-333`); later iterations use the configured strategy.
 """
 
+import gc
 import os
 import time
 from typing import Callable, List, Optional
@@ -345,8 +346,18 @@ class ChunkTrainer:
         graph = torch.cuda.CUDAGraph()
         n0 = _native.launch_count()
         ex.record_k1, n_ev = True, len(ex.k1_events)
-        with torch.cuda.graph(graph, stream=self._side):
-            self._static_loss = self._eager_step(self._static_tokens)
+        # no cyclic GC inside the capture: collecting an unrelated dead object
+        # that owns CUDA resources (another trainer's events, graphs, pinned
+        # buffers) would issue CUDA calls that invalidate a global-mode capture
+        gc_was_enabled = gc.isenabled()
+        gc.collect()
+        gc.disable()
+        try:
+            with torch.cuda.graph(graph, stream=self._side):
+                self._static_loss = self._eager_step(self._static_tokens)
+        finally:
+            if gc_was_enabled:
+                gc.enable()
         self.graph_kernels_per_step = _native.launch_count() - n0
         # event-record nodes of the graph reference these events: they live with it
         self._graph_events = ex.k1_events[n_ev:]
