@@ -14,6 +14,7 @@ after the collective (no host wait), like torch's NCCL work objects.
 """
 
 import ctypes
+import sys
 from typing import List, Optional, Tuple
 
 import torch
@@ -68,6 +69,10 @@ class NativeChunkComm:
             self._comm = ctypes.c_void_p()
 
     def __del__(self):
+        # at interpreter exit the CUDA context may already be gone: leave the
+        # communicator to the process teardown rather than call into NCCL
+        if sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
