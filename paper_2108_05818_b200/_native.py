@@ -71,6 +71,10 @@ SIGNATURES = {
     "cs_adam_chunks_host": (ctypes.c_int, [ctypes.POINTER(CsAdamItem), ctypes.c_int,
                                            ctypes.c_int, ctypes.POINTER(CsAdamHyper),
                                            ctypes.POINTER(CsStepState), ctypes.c_int]),
+    "cs_adam_chunks_host_oop": (ctypes.c_int, [ctypes.POINTER(CsAdamItem),
+                                               ctypes.POINTER(CsAdamItem), ctypes.c_int,
+                                               ctypes.c_int, ctypes.POINTER(CsAdamHyper),
+                                               ctypes.POINTER(CsStepState), ctypes.c_int]),
     "cs_grad_sumsq_host": (ctypes.c_int, [ctypes.POINTER(CsGradItem), ctypes.c_int, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_double), ctypes.c_int]),
     "cs_embed_fwd_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
