@@ -81,7 +81,7 @@ class ChunkTrainer:
                  gather_depth: int = 2, embedding_placement: str = "plan",
                  untied_head: Optional[bool] = None,
                  async_host_adam: Optional[bool] = None,
-                 comm=None):
+                 comm=None, speculative_host_adam: Optional[bool] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -122,6 +122,8 @@ class ChunkTrainer:
         ex = self.executor
         if async_host_adam is not None:
             ex.async_host_adam = async_host_adam
+        if speculative_host_adam is not None:
+            ex.speculative_host_adam = speculative_host_adam
         self.tracer = None
         if non_model == "measured" and non_model_fn is None:
             from .tracer import MemoryTracer
@@ -132,6 +134,7 @@ class ChunkTrainer:
                              payload_backend=ex, collective_backend=ex, executor=ex,
                              non_model_fn=non_model_fn)
         self.nproc, self.rank = nproc, rank
+        ex.set_timeline(self.sim.timeline)
         # where the embedding operator physically runs: the reference's plan
         # (`profiler.py:70-74`, set on the engine by the Simulator) unless forced
         if embedding_placement == "plan":
