@@ -45,8 +45,9 @@ __attribute__((target("avx2,fma,f16c"))) inline void store16(uint16_t* p, __m256
   _mm_storeu_si128(reinterpret_cast<__m128i*>(p), h);
 }
 
-// in: g16 (gradients), p32, m, v; out: o16, o32, om, ov (may alias the inputs)
-template <int DT>
+// in: g16 (gradients), p32, m, v; out: o16, o32, om, ov (may alias the inputs
+// unless STREAM; STREAM needs 32-byte aligned fp32 and 16-byte aligned fp16 outputs)
+template <int DT, bool STREAM = false>
 __attribute__((target("avx2,fma,f16c"))) inline void adam8_oop(
     const uint16_t* g16, const float* p32, const float* m, const float* v, uint16_t* o16,
     float* o32, float* om, float* ov, const Consts& c) {
@@ -62,10 +63,20 @@ __attribute__((target("avx2,fma,f16c"))) inline void adam8_oop(
                                     _mm256_mul_ps(_mm256_loadu_ps(v), c.b2));
   const __m256 denom = _mm256_add_ps(_mm256_div_ps(_mm256_sqrt_ps(vv), c.sb), c.eps);
   p = _mm256_add_ps(p, _mm256_div_ps(_mm256_mul_ps(c.nss, mm), denom));
-  _mm256_storeu_ps(o32, p);
-  _mm256_storeu_ps(om, mm);
-  _mm256_storeu_ps(ov, vv);
-  store16<DT>(o16, p);
+  if (STREAM) {  // fresh output lines: non-temporal stores skip the read-for-ownership
+    _mm256_stream_ps(o32, p);
+    _mm256_stream_ps(om, mm);
+    _mm256_stream_ps(ov, vv);
+    alignas(16) uint16_t h[8];
+    store16<DT>(h, p);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(o16),
+                     _mm_load_si128(reinterpret_cast<const __m128i*>(h)));
+  } else {
+    _mm256_storeu_ps(o32, p);
+    _mm256_storeu_ps(om, mm);
+    _mm256_storeu_ps(ov, vv);
+    store16<DT>(o16, p);
+  }
 }
 
 template <int DT>
@@ -75,9 +86,18 @@ __attribute__((target("avx2,fma,f16c"))) void adam_range_oop(const CsAdamItem& i
   const uint16_t* g16 = static_cast<const uint16_t*>(in.p16);
   uint16_t* o16 = static_cast<uint16_t*>(out.p16);
   int64_t e = lo;
-  for (; e + 8 <= hi; e += 8)
-    adam8_oop<DT>(g16 + e, in.p32 + e, in.m + e, in.v + e, o16 + e, out.p32 + e, out.m + e,
-                  out.v + e, c);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(out.p32) | reinterpret_cast<uintptr_t>(out.m) |
+                         reinterpret_cast<uintptr_t>(out.v)) & 31) == 0 &&
+                       (reinterpret_cast<uintptr_t>(o16) & 15) == 0 && (lo & 7) == 0;
+  if (aligned) {
+    for (; e + 8 <= hi; e += 8)
+      adam8_oop<DT, true>(g16 + e, in.p32 + e, in.m + e, in.v + e, o16 + e, out.p32 + e,
+                          out.m + e, out.v + e, c);
+  } else {
+    for (; e + 8 <= hi; e += 8)
+      adam8_oop<DT>(g16 + e, in.p32 + e, in.m + e, in.v + e, o16 + e, out.p32 + e, out.m + e,
+                    out.v + e, c);
+  }
   if (e < hi) {  // tail: the same 8-lane code on a padded copy
     alignas(32) uint16_t t16[8] = {0};
     alignas(32) float tp[8] = {0}, tm[8] = {0}, tv[8] = {0};
@@ -246,13 +266,17 @@ extern "C" int cs_adam_chunks_host_oop(const CsAdamItem* in, const CsAdamItem* o
   }
   const int64_t nr = (int64_t)ranges.size();
   const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
-#pragma omp parallel for num_threads(threads) schedule(static)
-  for (int64_t r = 0; r < nr; ++r) {
-    const int i = ranges[r].first;
-    const int64_t lo = ranges[r].second;
-    const int64_t hi = lo + kRange < in[i].n ? lo + kRange : in[i].n;
-    if (dtype == CS_FP16) adam_range_oop<CS_FP16>(in[i], out[i], lo, hi, c);
-    else adam_range_oop<CS_BF16>(in[i], out[i], lo, hi, c);
+#pragma omp parallel num_threads(threads)
+  {
+#pragma omp for schedule(static)
+    for (int64_t r = 0; r < nr; ++r) {
+      const int i = ranges[r].first;
+      const int64_t lo = ranges[r].second;
+      const int64_t hi = lo + kRange < in[i].n ? lo + kRange : in[i].n;
+      if (dtype == CS_FP16) adam_range_oop<CS_FP16>(in[i], out[i], lo, hi, c);
+      else adam_range_oop<CS_BF16>(in[i], out[i], lo, hi, c);
+    }
+    _mm_sfence();  // each thread's non-temporal stores are visible before the join
   }
   return 0;
 }

@@ -195,10 +195,12 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         #: scalars match bit for bit; otherwise they are dropped and the normal
         #: update runs.  Single rank only (at p > 1 the reduce-scatter comes first).
         #: Off by default: bit-identical (tests), but measured SLOWER on the
-        #: 16-core B200 hosts — 1B with every triplet on the host 389-404 vs
-        #: 348-362 ms/step, 12B mixed 2.22 vs 2.04 s — because the async host
+        #: 16-core B200 hosts — 1B with every triplet on the host 361-407 vs
+        #: 353-354 ms/step, 12B mixed 2.30 vs 2.04 s
+        #: (profiles/r01/speculative_host_adam_ab.txt) — because the async host
         #: Adam already overlaps the next forward, and an update running beside
-        #: the backward's enqueue and D2Hs streams at 3.5 instead of 5.2 Gelem/s.
+        #: the backward's enqueue and D2Hs streams at 4.4-4.6 instead of 5.3
+        #: Gelem/s even with non-temporal stores into the shadows.
         self.speculative_host_adam = os.environ.get("CS_SPEC_HOST_ADAM", "0") == "1"
         self.spec_max_positions = int(os.environ.get("CS_SPEC_MAX_POSITIONS", "64"))
         # OpenMP threads of a speculative update (0: all cores; fewer measured
