@@ -97,7 +97,17 @@ xent_fwd_kernel(const uint16_t* __restrict__ logits, const int64_t* __restrict__
     const uint4* xv = reinterpret_cast<const uint4*>(x);
     const int64_t nv = vocab / 8;
     int64_t i = threadIdx.x;
-    for (; i + kThreads < nv; i += 2 * kThreads) {  // two 128-bit loads in flight
+    for (; i + 3 * kThreads < nv; i += 4 * kThreads) {  // four 128-bit loads in flight
+      const uint4 w0 = __ldcs(xv + i);
+      const uint4 w1 = __ldcs(xv + i + kThreads);
+      const uint4 w2 = __ldcs(xv + i + 2 * kThreads);
+      const uint4 w3 = __ldcs(xv + i + 3 * kThreads);
+      online8<DT>(w0, m, s);
+      online8<DT>(w1, m, s);
+      online8<DT>(w2, m, s);
+      online8<DT>(w3, m, s);
+    }
+    for (; i + kThreads < nv; i += 2 * kThreads) {
       const uint4 w0 = __ldcs(xv + i);
       const uint4 w1 = __ldcs(xv + i + kThreads);
       online8<DT>(w0, m, s);
