@@ -17,7 +17,7 @@
 
 namespace {
 
-constexpr int kWarps = 8;       // rows per CTA
+constexpr int kWarps = 4;       // rows per CTA (4: 5 CTAs = 20 rows in flight per SM at 90 regs; 8: 16)
 
 template <int DT>
 __device__ __forceinline__ float to_f(uint16_t h) {
