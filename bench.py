@@ -384,6 +384,8 @@ def main():
     # ---- timed region 1: device-resident inputs -> value -----------------------
     ex.record_k1 = True
     ex.k1_events.clear()
+    moved0 = ex.stats.h2d_bytes - ex.stats.prefetch_discarded_bytes + ex.stats.d2h_bytes
+    reports0 = len(trainer.reports)
     launches0 = _native.launch_count()
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -404,6 +406,11 @@ def main():
     if trainer._graph is not None:  # library kernels replayed from the captured graph
         launches += trainer.graph_kernels_per_step * args.steps
     ms = t0.elapsed_time(t1) / args.steps
+    # chunk bytes the executor moved in the timed steps (a replayed graph
+    # moves none: it is only captured once the schedule moves no chunk)
+    moved = (ex.stats.h2d_bytes - ex.stats.prefetch_discarded_bytes + ex.stats.d2h_bytes
+             - moved0) / args.steps
+    billed = [r.pcie_bytes for r in trainer.reports[reports0:reports0 + args.steps]]
     ex.record_k1 = False
     k1_ms = [a.elapsed_time(b) for a, b, _ in ex.k1_events]
     k1_elems = [n for _, _, n in ex.k1_events]
@@ -492,6 +499,16 @@ def main():
                 "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_ms, 3),
                 "device_ms_per_step": round(e2e_dev_ms, 3),
                 "sm_mhz": clk2.get("sm_mhz")},
+        "pcie_per_step": {
+            "ledger_billed_bytes": int(sum(billed) / max(len(billed), 1)),
+            "physically_moved_chunk_bytes": int(moved),
+            "ledger_rows_not_realized": trainer.ledger_rows_not_realized(),
+            "note": "the reference bills a GPU-computed embedding's weights down at FWD and "
+                    "weight grads up at BWD (engine.py:214-219); here they stay resident in "
+                    "HBM, charged to the GPU pool (DESIGN.md section 7)"},
+        "gpu_resident_non_chunked_bytes": trainer.gpu_resident_bytes,
+        "non_model": "measured" if trainer.tracer is not None else "analytic",
+        "host_threads": trainer.host_threads,
         "gpu_launches": int(launches),
         "host_enqueue_ms_per_step": round(host_ms, 3),
         "cuda_graph": trainer._graph is not None,

@@ -51,7 +51,8 @@ enum {
   CS_EINVAL = -1,      /* bad argument (null pointer, negative count, dtype) */
   CS_EALIGN = -2,      /* a vectorised buffer is not 16-byte aligned */
   CS_ETOOMANY = -3,    /* work list longer than CS_MAX_ITEMS */
-  CS_EUNAVAIL = -4     /* NCCL could not be loaded (cs_comm_* / collectives) */
+  CS_EUNAVAIL = -4,    /* NCCL could not be loaded (cs_comm_* / collectives) */
+  CS_EINPROGRESS = -5  /* cs_comm_check: a nonblocking NCCL operation is pending */
 };
 
 #define CS_MAX_ITEMS 4096
@@ -113,6 +114,13 @@ const char* cs_last_error(void);
 int64_t     cs_launch_count(void);
 /* number of SMs of the current device (grid sizing), or <0 on error */
 int         cs_num_sms(void);
+/* OpenMP team size the host kernels use for n_threads = requested:
+ * requested if > 0, else (cores in this process's affinity mask) /
+ * $LOCAL_WORLD_SIZE (one process per GPU shares the host with its local
+ * peers; the division is skipped when CS_HOST_BOUND=1 says the mask is
+ * already this rank's own share), at least 1.  Never omp_get_max_threads():
+ * torchrun sets OMP_NUM_THREADS=1. */
+int         cs_host_threads(int requested);
 
 /* ---- K1: fused chunk Adam -------------------------------------------------
  * Replaces the accounting of Engine._adam_event for a GPU-placed position
@@ -124,13 +132,11 @@ int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
                    const CsAdamHyper* hyper, const CsStepState* d_state,
                    void* stream);
 /* Tuning: select K1's data-movement variant (bit-identical results):
- * 0-4 SIMT register-tiled (groups/thread x min CTAs/SM), 5-7 TMA-staged
- * (cp.async.bulk + mbarrier ring), 8-24 TMA-staged with a dedicated
- * bulk-store warp (tile size x stages x consumer warps; table in adam.cu,
- * A/B results in profiles/r01/k1_variants.md).  v < 0 only queries.
- * Default from $CS_ADAM_VARIANT, else 21 (5120-element tiles x 3 stages,
- * 20 consumer warps).  Items whose pointers are not 16-byte aligned run on
- * variant 0. */
+ * 0 SIMT register-tiled, 1 TMA-staged (cp.async.bulk + mbarrier ring with a
+ * dedicated bulk-store warp; 5120-element tiles x 3 stages, 20 consumer
+ * warps).  v < 0 only queries.  Default from $CS_ADAM_VARIANT, else 1.
+ * Items whose pointers are not 16-byte aligned always run on variant 0.
+ * The round-1 sweep of 25 tilings: profiles/r01/k1_variants.md. */
 int cs_adam_variant(int v);
 
 /* ---- K2: gradient sum of squares -------------------------------------------
@@ -178,17 +184,13 @@ int cs_master_init(float* p32, float* m, float* v, const void* src, int src_dtyp
  * (`profiler.py:93-130`); the reference then moves grads D2H and new params
  * H2D as `adam_copy` (`engine.py:249-251, 265-267`).  This is the host
  * kernel that runs there (AVX2/F16C + OpenMP, same rounding as K1).
- * `state` is a HOST copy of the step scalars. Synchronous. */
+ * `state` is a HOST copy of the step scalars. Synchronous.
+ * n_threads (here and in every host entry below): > 0 uses exactly that
+ * many OpenMP threads; 0 uses cs_host_threads(0), this process's share of
+ * the host cores. */
 int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
                         const CsAdamHyper* hyper, const CsStepState* state,
                         int n_threads);
-
-/* Out-of-place host Adam: in[i] = (gradients in p16, p32, m, v) are read,
- * out[i] = (p16, p32, m, v) receive the update (same bits as the in-place
- * call).  For a speculative update that may be discarded: the inputs stay
- * intact.  in[i].n == out[i].n; state->skip must be 0. */
-int cs_adam_chunks_host_oop(const CsAdamItem* in, const CsAdamItem* out, int n_items, int dtype,
-                            const CsAdamHyper* hyper, const CsStepState* state, int n_threads);
 
 /* Host sum of squares (double accumulation) of fp16/bf16 gradients that sit
  * in host DRAM (grads of a chunk evicted to the CPU before the ADAM event,
@@ -286,6 +288,14 @@ int cs_reduce_scatter_avg(void* local, const void* group_buf, int64_t count, int
                           void* comm, void* stream);
 /* replicated (non-chunked) grads: avg=1; the global sum of squares: avg=0, CS_FP32 */
 int cs_allreduce(void* buf, int64_t count, int dtype, int avg, void* comm, void* stream);
+/* Failure detection (surface NCCL async errors): 0 while the
+ * communicator is healthy, CS_EINPROGRESS while a nonblocking operation is
+ * pending, else the asynchronous ncclResult_t of a collective that failed
+ * after it was enqueued (ncclCommGetAsyncError).  Poll while waiting. */
+int cs_comm_check(void* comm);
+/* ncclCommAbort: tear down without waiting for outstanding collectives
+ * (unblocks kernels stuck on a dead peer); the handle is invalid after. */
+int cs_comm_abort(void* comm);
 
 #ifdef __cplusplus
 }

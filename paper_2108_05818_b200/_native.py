@@ -11,6 +11,7 @@ from typing import Optional
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libchunkstar_b200.so")
 
 CS_FP16, CS_BF16, CS_FP32 = 0, 1, 2
+CS_EINVAL, CS_EALIGN, CS_ETOOMANY, CS_EUNAVAIL, CS_EINPROGRESS = -1, -2, -3, -4, -5
 
 
 class CsAdamHyper(ctypes.Structure):
@@ -47,6 +48,7 @@ SIGNATURES = {
     "cs_version": (ctypes.c_char_p, []),
     "cs_last_error": (ctypes.c_char_p, []),
     "cs_launch_count": (ctypes.c_int64, []),
+    "cs_host_threads": (ctypes.c_int, [ctypes.c_int]),
     "cs_num_sms": (ctypes.c_int, []),
     "cs_adam_chunks": (ctypes.c_int, [ctypes.POINTER(CsAdamItem), ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(CsAdamHyper), ctypes.c_void_p,
@@ -71,10 +73,6 @@ SIGNATURES = {
     "cs_adam_chunks_host": (ctypes.c_int, [ctypes.POINTER(CsAdamItem), ctypes.c_int,
                                            ctypes.c_int, ctypes.POINTER(CsAdamHyper),
                                            ctypes.POINTER(CsStepState), ctypes.c_int]),
-    "cs_adam_chunks_host_oop": (ctypes.c_int, [ctypes.POINTER(CsAdamItem),
-                                               ctypes.POINTER(CsAdamItem), ctypes.c_int,
-                                               ctypes.c_int, ctypes.POINTER(CsAdamHyper),
-                                               ctypes.POINTER(CsStepState), ctypes.c_int]),
     "cs_grad_sumsq_host": (ctypes.c_int, [ctypes.POINTER(CsGradItem), ctypes.c_int, ctypes.c_int,
                                           ctypes.POINTER(ctypes.c_double), ctypes.c_int]),
     "cs_embed_fwd_host": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
@@ -125,6 +123,8 @@ SIGNATURES = {
                                              ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_allreduce": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p, ctypes.c_void_p]),
+    "cs_comm_check": (ctypes.c_int, [ctypes.c_void_p]),
+    "cs_comm_abort": (ctypes.c_int, [ctypes.c_void_p]),
 }
 
 _lib: Optional[ctypes.CDLL] = None

@@ -33,14 +33,15 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kGroups = 4;   // 4-element groups per thread per block tile (K2)
 constexpr int kSumsqTile = kThreads * kGroups * 8;  // K2: 128-bit groups
-// K1 tiling variants (groups per thread, min resident CTAs per SM -> register
-// cap).  Selected once per process (CS_ADAM_VARIANT, default kAdamDefault);
-// every variant computes bit-identical results.
-struct AdamVariant { int groups, min_blocks; };
-constexpr AdamVariant kAdamVariants[] = {{4, 1}, {4, 4}, {2, 4}, {2, 6}, {8, 2}};
-constexpr int kAdamSimtVariants = 5;   // 5..24 = TMA-staged variants (adam_tma.cu)
-constexpr int kAdamVariantCount = 25;
-constexpr int kAdamDefault = 21;  // TMA-staged, 20 consumer warps, 5120 x 3 stages
+// K1 data-movement variants, bit-identical results.  Selected once per
+// process (CS_ADAM_VARIANT, default kAdamDefault):
+//   0  SIMT register-tiled (this file; also the fallback for items whose
+//      streams are not 16-byte aligned)
+//   1  TMA-staged three-role pipeline (adam_tma.cu), the default
+// The round-1 sweep over 25 tilings is recorded in profiles/r01/k1_variants.md.
+constexpr int kAdamSimtGroups = 4;   // 4-element groups per thread per block tile
+constexpr int kAdamVariantCount = 2;
+constexpr int kAdamDefault = 1;
 
 struct AdamBatch {
   CsAdamItem item[cs::kMaxBatch];
@@ -344,17 +345,6 @@ int g_adam_blocks_per_sm = 0;
 
 typedef void (*AdamKernel)(const AdamBatch, const CsStepState*);
 
-template <int DT>
-AdamKernel adam_kernel_for(int v) {
-  switch (v) {
-    case 1: return adam_chunks_kernel<DT, 4, 4>;
-    case 2: return adam_chunks_kernel<DT, 2, 4>;
-    case 3: return adam_chunks_kernel<DT, 2, 6>;
-    case 4: return adam_chunks_kernel<DT, 8, 2>;
-    default: return adam_chunks_kernel<DT, 4, 1>;
-  }
-}
-
 int adam_variant() {
   if (g_adam_variant < 0) {
     const char* e = getenv("CS_ADAM_VARIANT");
@@ -387,7 +377,7 @@ int launch_error(const char* what) {
 }  // namespace
 
 int cs_adam_chunks_tma(const CsAdamItem* items, int n_items, int dtype, const CsAdamHyper* h,
-                       const CsStepState* d_state, void* stream, int variant);
+                       const CsStepState* d_state, void* stream);
 
 extern "C" int cs_num_sms(void) { return num_sms(); }
 
@@ -412,13 +402,16 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
     cs::set_error("cs_adam_chunks: invalid argument");
     return CS_EINVAL;
   }
+  if (n_items > CS_MAX_ITEMS) {
+    cs::set_error("cs_adam_chunks: %d items > CS_MAX_ITEMS", n_items);
+    return CS_ETOOMANY;
+  }
   const int sms = num_sms();
   if (sms <= 0) {
     cs::set_error("cs_adam_chunks: no CUDA device");
     return CS_EINVAL;
   }
-  int variant = adam_variant();
-  if (variant >= kAdamSimtVariants) {
+  if (adam_variant() == 1) {
     bool ok16 = true;
     for (int i = 0; i < n_items && ok16; ++i)
       ok16 = aligned(items[i].p16, 16) && aligned(items[i].p32, 16) && aligned(items[i].m, 16) &&
@@ -431,24 +424,25 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
           return CS_EINVAL;
         }
       }
-      return cs_adam_chunks_tma(items, n_items, dtype, hyper, d_state, stream, variant);
+      return cs_adam_chunks_tma(items, n_items, dtype, hyper, d_state, stream);
     }
-    variant = 0;  // bulk copies need 16-byte aligned streams: the SIMT kernel takes the rest
+    // bulk copies need 16-byte aligned streams: the SIMT kernel takes the rest
   }
-  const int64_t tile_elems = (int64_t)kThreads * kAdamVariants[variant].groups * 4;
-  AdamKernel kern = dtype == CS_FP16 ? adam_kernel_for<CS_FP16>(variant)
-                                     : adam_kernel_for<CS_BF16>(variant);
+  const int64_t tile_elems = (int64_t)kThreads * kAdamSimtGroups * 4;
+  AdamKernel kern = dtype == CS_FP16 ? adam_chunks_kernel<CS_FP16, kAdamSimtGroups, 1>
+                                     : adam_chunks_kernel<CS_BF16, kAdamSimtGroups, 1>;
   if (g_adam_blocks_per_sm == 0) {
     int nb = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, 0);
     g_adam_blocks_per_sm = nb > 0 ? nb : 1;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int first = 0; first < n_items; first += cs::kMaxBatch) {
+  for (int first = 0; first < n_items;) {
     AdamBatch b;
     b.n = 0;
     int64_t tiles = 0;
-    for (int i = first; i < n_items && b.n < cs::kMaxBatch; ++i) {
+    int i = first;
+    for (; i < n_items && b.n < cs::kMaxBatch; ++i) {
       const CsAdamItem& it = items[i];
       if (it.n < 0 || (it.n > 0 && (!it.p16 || !it.p32 || !it.m || !it.v))) {
         cs::set_error("cs_adam_chunks: item %d invalid", i);
@@ -459,12 +453,13 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
         cs::set_error("cs_adam_chunks: item %d misaligned (p16 needs 8 B, fp32 16 B)", i);
         return CS_EALIGN;
       }
-      if (it.n == 0) continue;
+      if (it.n == 0) continue;  // takes no batch slot
       b.item[b.n] = it;
       b.tile_start[b.n] = tiles;
       tiles += (it.n + tile_elems - 1) / tile_elems;
       ++b.n;
     }
+    first = i;  // resume where this batch stopped
     b.tile_start[b.n] = tiles;
     if (b.n == 0) continue;
     b.b2 = (float)hyper->beta2;
@@ -490,6 +485,10 @@ extern "C" int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
     cs::set_error("cs_grad_sumsq: invalid argument");
     return CS_EINVAL;
   }
+  if (n_items > CS_MAX_ITEMS) {
+    cs::set_error("cs_grad_sumsq: %d items > CS_MAX_ITEMS", n_items);
+    return CS_ETOOMANY;
+  }
   const int grid = cs_sumsq_partials();
   if (grid <= 0) {
     cs::set_error("cs_grad_sumsq: no CUDA device");
@@ -503,7 +502,8 @@ extern "C" int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
     b.n = 0;
     b.accumulate = wrote ? 1 : 0;
     int64_t tiles = 0;
-    for (int i = first; i < n_items && b.n < cs::kMaxBatch; ++i) {
+    int i = first;
+    for (; i < n_items && b.n < cs::kMaxBatch; ++i) {
       const CsGradItem& it = items[i];
       if (it.n < 0 || (it.n > 0 && !it.g16)) {
         cs::set_error("cs_grad_sumsq: item %d invalid", i);
@@ -513,12 +513,13 @@ extern "C" int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
         cs::set_error("cs_grad_sumsq: item %d misaligned", i);
         return CS_EALIGN;
       }
-      if (it.n == 0) continue;
+      if (it.n == 0) continue;  // takes no batch slot
       b.item[b.n] = it;
       b.tile_start[b.n] = tiles;
       tiles += (it.n + kSumsqTile - 1) / kSumsqTile;
       ++b.n;
     }
+    first = i;  // resume where this batch stopped
     b.tile_start[b.n] = tiles;
     // launched even when empty so the partials are (re)initialised
     if (dtype == CS_FP16)
@@ -528,7 +529,6 @@ extern "C" int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
     cs::note_launches(1);
     if (int e = launch_error("cs_grad_sumsq")) return e;
     wrote = true;
-    first += cs::kMaxBatch;
   } while (first < n_items);
   return 0;
 }

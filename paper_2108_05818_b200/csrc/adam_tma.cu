@@ -1,21 +1,21 @@
-// K1 fused chunk Adam, TMA-staged variant (sm_100a).
+// K1 fused chunk Adam, TMA-staged (sm_100a) -- the default K1.
 //
 // Same arithmetic as adam_chunks_kernel (adam.cu, bit-identical results);
 // different data movement.  A persistent CTA per SM runs a STAGES-deep ring
-// of shared-memory tiles:
+// of shared-memory tiles with three roles:
 //
 //   producer (one lane)   : wait empty[s] -> mbarrier expect_tx(14·T bytes) ->
 //                           cp.async.bulk global->shared of the tile's g16,
 //                           p32, m, v (4 bulk copies, complete_tx on full[s])
-//   consumers (8 warps)   : wait full[s] -> Adam in shared memory, in place
-//                           (p16 written over the g16 slot) -> named barrier ->
-//                           one lane: fence.proxy.async, cp.async.bulk
-//                           shared->global of p16, p32, m, v, commit, wait
-//                           until the bulk reads of the stage are done ->
-//                           arrive empty[s]
+//   consumers (CW warps)  : wait full[s] -> Adam in shared memory, in place
+//                           (p16 written over the g16 slot) -> fence.proxy.async
+//                           -> arrive computed[s] and move on to the next tile
+//   store warp (one lane) : wait computed[s] -> cp.async.bulk shared->global of
+//                           p16, p32, m, v, commit; once the bulk reads of the
+//                           previous group are done -> arrive empty[s]
 //
 // Loads for STAGES tiles are always in flight while the consumers compute and
-// the stores drain asynchronously, so the SM keeps ~STAGES·28 KB of read
+// the stores drain asynchronously, so the SM keeps ~STAGES·14·T bytes of read
 // traffic outstanding with a handful of registers.  Tiles are T elements of
 // one item (the used prefix of one chunk position); each item's last n % 8
 // elements (bulk copies move multiples of 16 B) are updated by the consumer
@@ -28,10 +28,6 @@
 #include "cs_internal.h"
 
 namespace cs_tma {
-
-constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kThreads = kConsumers + 32;  // + one producer warp
 
 struct Batch {
   CsAdamItem item[cs::kMaxBatch];
@@ -135,132 +131,6 @@ __device__ __forceinline__ int find_item(const int64_t* start, int n, int64_t ti
     if (start[mid] <= tile) lo = mid; else hi = mid - 1;
   }
   return lo;
-}
-
-template <int DT, int T, int STAGES>
-__global__ void __launch_bounds__(kThreads)
-adam_tma_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict__ st) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int kStageBytes = T * 14;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
-  uint64_t* empty = full + STAGES;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (st->skip) {  // non-finite gradients: no update, p16 = round(p32) restored
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int i = 0; i < b.n; ++i) {
-      const CsAdamItem it = b.item[i];
-      uint16_t* q16 = static_cast<uint16_t*>(it.p16);
-      for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < it.n; e += stride)
-        q16[e] = from_f<DT>(it.p32[e]);
-    }
-    return;
-  }
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int64_t total = b.tile_start[b.n];
-
-  if (warp == kConsumerWarps) {  // ---- producer warp
-    if (lane == 0) {
-      int64_t k = 0;
-      for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++k) {
-        const int s = (int)(k % STAGES);
-        const uint32_t phase = (uint32_t)((k / STAGES) & 1);
-        mbar_wait(&empty[s], phase ^ 1u);
-        const int i = find_item(b.tile_start, b.n, tile);
-        const CsAdamItem it = b.item[i];
-        const int64_t e0 = (tile - b.tile_start[i]) * T;
-        const int64_t nvec = it.n & ~(int64_t)7;
-        const int len = (int)((nvec - e0) < T ? (nvec - e0) : T);
-        unsigned char* base = smem + s * kStageBytes;
-        mbar_expect_tx(&full[s], (uint32_t)len * 14u);
-        bulk_load(base, static_cast<const uint16_t*>(it.p16) + e0, len * 2, &full[s]);
-        bulk_load(base + T * 2, it.p32 + e0, len * 4, &full[s]);
-        bulk_load(base + T * 6, it.m + e0, len * 4, &full[s]);
-        bulk_load(base + T * 10, it.v + e0, len * 4, &full[s]);
-      }
-    }
-    return;
-  }
-
-  // ---- consumer warps
-  Consts c;
-  c.gs = st->grad_scale;
-  c.nss = -st->step_size;
-  c.sb = st->sqrt_bc2;
-  c.rsb = __ddiv_rn(1.0, (double)c.sb);
-  c.b2 = b.b2;
-  c.c1 = b.c1;
-  c.c2 = b.c2;
-  c.eps = b.eps;
-  c.wd = b.wd;
-  c.decay = b.decay;
-  c.adamw = b.adamw != 0;
-  const int t = threadIdx.x;
-  int64_t k = 0;
-  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x, ++k) {
-    const int s = (int)(k % STAGES);
-    const uint32_t phase = (uint32_t)((k / STAGES) & 1);
-    const int i = find_item(b.tile_start, b.n, tile);
-    const CsAdamItem it = b.item[i];
-    const int64_t e0 = (tile - b.tile_start[i]) * T;
-    const int64_t nvec = it.n & ~(int64_t)7;
-    const int len = (int)((nvec - e0) < T ? (nvec - e0) : T);
-    unsigned char* base = smem + s * kStageBytes;
-    uint16_t* g16 = reinterpret_cast<uint16_t*>(base);
-    float* p = reinterpret_cast<float*>(base + T * 2);
-    float* m = reinterpret_cast<float*>(base + T * 6);
-    float* v = reinterpret_cast<float*>(base + T * 10);
-    mbar_wait(&full[s], phase);
-    for (int e = t * 4; e < len; e += kConsumers * 4) {
-      uint2 gw = *reinterpret_cast<uint2*>(g16 + e);
-      float4 pp = *reinterpret_cast<float4*>(p + e);
-      float4 mm = *reinterpret_cast<float4*>(m + e);
-      float4 vv = *reinterpret_cast<float4*>(v + e);
-      adam1(to_f<DT>(gw.x & 0xffff), pp.x, mm.x, vv.x, c);
-      adam1(to_f<DT>(gw.x >> 16), pp.y, mm.y, vv.y, c);
-      adam1(to_f<DT>(gw.y & 0xffff), pp.z, mm.z, vv.z, c);
-      adam1(to_f<DT>(gw.y >> 16), pp.w, mm.w, vv.w, c);
-      *reinterpret_cast<float4*>(p + e) = pp;
-      *reinterpret_cast<float4*>(m + e) = mm;
-      *reinterpret_cast<float4*>(v + e) = vv;
-      gw.x = (uint32_t)from_f<DT>(pp.x) | ((uint32_t)from_f<DT>(pp.y) << 16);
-      gw.y = (uint32_t)from_f<DT>(pp.z) | ((uint32_t)from_f<DT>(pp.w) << 16);
-      *reinterpret_cast<uint2*>(g16 + e) = gw;
-    }
-    // make this thread's shared-memory writes visible to the async (bulk copy) proxy
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
-    if (t == 0) {
-      bulk_store(static_cast<uint16_t*>(it.p16) + e0, g16, len * 2);
-      bulk_store(it.p32 + e0, p, len * 4);
-      bulk_store(it.m + e0, m, len * 4);
-      bulk_store(it.v + e0, v, len * 4);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      mbar_arrive(&empty[s]);
-    }
-  }
-  // ragged tails (n % 8 elements per item), straight from global memory
-  for (int i = blockIdx.x; i < b.n; i += gridDim.x) {
-    const CsAdamItem it = b.item[i];
-    const int64_t e = (it.n & ~(int64_t)7) + t;
-    if (t < 8 && e < it.n) {
-      uint16_t* q16 = static_cast<uint16_t*>(it.p16);
-      float pp = it.p32[e], mm = it.m[e], vv = it.v[e];
-      adam1(to_f<DT>(q16[e]), pp, mm, vv, c);
-      it.p32[e] = pp;
-      it.m[e] = mm;
-      it.v[e] = vv;
-      q16[e] = from_f<DT>(pp);
-    }
-  }
-  if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Three-role variant: producer warp (bulk loads), 8 consumer warps (math),
@@ -433,33 +303,31 @@ adam_tma3_kernel(const __grid_constant__ Batch b, const CsStepState* __restrict_
   }
 }
 
-template <int DT, int T, int STAGES, bool THREE = false, int CW = 8, int U = 1>
+template <int DT, int T, int STAGES, int CW, int U = 1>
 int launch(const CsAdamItem* items, int n_items, const CsAdamHyper* h,
            const CsStepState* d_state, cudaStream_t stream, int ctas_per_sm) {
   constexpr int kSmem = STAGES * T * 14 + 3 * STAGES * 8;
   static bool configured = false;
   if (!configured) {
-    if (THREE)
-      cudaFuncSetAttribute(adam_tma3_kernel<DT, T, STAGES, CW, U>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    else
-      cudaFuncSetAttribute(adam_tma_kernel<DT, T, STAGES>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(adam_tma3_kernel<DT, T, STAGES, CW, U>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     configured = true;
   }
   const int sms = cs_num_sms();
-  for (int first = 0; first < n_items; first += cs::kMaxBatch) {
+  for (int first = 0; first < n_items;) {
     Batch b;
     b.n = 0;
     int64_t tiles = 0;
-    for (int i = first; i < n_items && b.n < cs::kMaxBatch; ++i) {
+    int i = first;
+    for (; i < n_items && b.n < cs::kMaxBatch; ++i) {
       const CsAdamItem& it = items[i];
-      if (it.n == 0) continue;
+      if (it.n == 0) continue;  // takes no batch slot
       b.item[b.n] = it;
       b.tile_start[b.n] = tiles;
       tiles += ((it.n & ~(int64_t)7) + T - 1) / T;
       ++b.n;
     }
+    first = i;  // resume where this batch stopped (zero-length items took no slot)
     b.tile_start[b.n] = tiles;
     if (b.n == 0) continue;
     b.b2 = (float)h->beta2;
@@ -472,10 +340,7 @@ int launch(const CsAdamItem* items, int n_items, const CsAdamHyper* h,
     int64_t grid = (int64_t)sms * ctas_per_sm;
     const int64_t need = tiles > b.n ? tiles : b.n;  // every item's tail needs a CTA
     if (grid > need) grid = need;
-    if (THREE)
-      adam_tma3_kernel<DT, T, STAGES, CW, U><<<(int)grid, CW * 32 + 64, kSmem, stream>>>(b, d_state);
-    else
-      adam_tma_kernel<DT, T, STAGES><<<(int)grid, kThreads, kSmem, stream>>>(b, d_state);
+    adam_tma3_kernel<DT, T, STAGES, CW, U><<<(int)grid, CW * 32 + 64, kSmem, stream>>>(b, d_state);
     cs::note_launches(1);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -488,99 +353,14 @@ int launch(const CsAdamItem* items, int n_items, const CsAdamHyper* h,
 
 }  // namespace cs_tma
 
-// Entry used by cs_adam_chunks for the TMA variants (see adam.cu).
+// Entry used by cs_adam_chunks for the TMA-staged K1 (variant 1, see adam.cu):
+// 5120-element tiles x 3 stages (215 KB of the 227 KB of shared memory),
+// 20 consumer warps, 1 CTA per SM.  The A/B sweep over tile size, stage count
+// and consumer warps that chose it is in profiles/r01/k1_variants.md.
 int cs_adam_chunks_tma(const CsAdamItem* items, int n_items, int dtype, const CsAdamHyper* h,
-                       const CsStepState* d_state, void* stream, int variant) {
+                       const CsStepState* d_state, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // variant 5: T=2048 x 4 stages (112 KB), 1 CTA/SM; 6: T=2048 x 3 (84 KB), 2 CTAs/SM;
-  // 7: T=4096 x 3 (168 KB), 1 CTA/SM; three-role: 8: T=2048 x 6 (168 KB) 1 CTA/SM,
-  // 9: T=2048 x 3, 2 CTAs/SM; 10: T=1024 x 4 (57 KB), 3 CTAs/SM
-  if (variant == 11) {  // 16 consumer warps, 2048 x 6 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 2048, 6, true, 16>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 22) {  // 24 consumer warps, 5120 x 3 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 5120, 3, true, 24>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 5120, 3, true, 24>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 23) {  // 24 consumer warps, 4096 x 3 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 4096, 3, true, 24>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 4096, 3, true, 24>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 24) {  // 28 consumer warps, 5120 x 3 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 5120, 3, true, 28>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 5120, 3, true, 28>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 20) {  // 16 consumer warps, 5120 x 3 stages (215 KB of the 227 KB)
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 5120, 3, true, 16>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 5120, 3, true, 16>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 21) {  // 20 consumer warps, 5120 x 3 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 5120, 3, true, 20>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 5120, 3, true, 20>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 18) {  // 16 consumer warps, 3072 x 4 stages (two stages of loads in flight)
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 3072, 4, true, 16>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 3072, 4, true, 16>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 19) {  // 16 consumer warps, 2560 x 5 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 2560, 5, true, 16>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 2560, 5, true, 16>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 16) {  // variant 12 with two 4-element groups per consumer pass
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 4096, 3, true, 16, 2>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 4096, 3, true, 16, 2>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 17) {  // 8 consumer warps, two groups per pass, 4096 x 3 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 4096, 3, true, 8, 2>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 4096, 3, true, 8, 2>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 12) {  // 16 consumer warps, 4096 x 3 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 4096, 3, true, 16>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 4096, 3, true, 16>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 15) {  // 12 consumer warps, 2048 x 6 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 2048, 6, true, 12>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 2048, 6, true, 12>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 14) {  // 16 consumer warps, 2048 x 7 stages
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 2048, 7, true, 16>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_BF16, 2048, 7, true, 16>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 13) {  // 12 consumer warps, 2048 x 3 stages, 2 CTAs/SM
-    if (dtype == CS_FP16)
-      return cs_tma::launch<CS_FP16, 2048, 3, true, 12>(items, n_items, h, d_state, s, 2);
-    return cs_tma::launch<CS_BF16, 2048, 3, true, 12>(items, n_items, h, d_state, s, 2);
-  }
-  if (variant >= 8) {
-    if (dtype == CS_FP16) {
-      if (variant == 8) return cs_tma::launch<CS_FP16, 2048, 6, true>(items, n_items, h, d_state, s, 1);
-      if (variant == 9) return cs_tma::launch<CS_FP16, 2048, 3, true>(items, n_items, h, d_state, s, 2);
-      return cs_tma::launch<CS_FP16, 1024, 4, true>(items, n_items, h, d_state, s, 3);
-    }
-    if (variant == 8) return cs_tma::launch<CS_BF16, 2048, 6, true>(items, n_items, h, d_state, s, 1);
-    if (variant == 9) return cs_tma::launch<CS_BF16, 2048, 3, true>(items, n_items, h, d_state, s, 2);
-    return cs_tma::launch<CS_BF16, 1024, 4, true>(items, n_items, h, d_state, s, 3);
-  }
-  if (dtype == CS_FP16) {
-    if (variant == 6) return cs_tma::launch<CS_FP16, 2048, 3>(items, n_items, h, d_state, s, 2);
-    if (variant == 7) return cs_tma::launch<CS_FP16, 4096, 3>(items, n_items, h, d_state, s, 1);
-    return cs_tma::launch<CS_FP16, 2048, 4>(items, n_items, h, d_state, s, 1);
-  }
-  if (variant == 6) return cs_tma::launch<CS_BF16, 2048, 3>(items, n_items, h, d_state, s, 2);
-  if (variant == 7) return cs_tma::launch<CS_BF16, 4096, 3>(items, n_items, h, d_state, s, 1);
-  return cs_tma::launch<CS_BF16, 2048, 4>(items, n_items, h, d_state, s, 1);
+  if (dtype == CS_FP16)
+    return cs_tma::launch<CS_FP16, 5120, 3, 20>(items, n_items, h, d_state, s, 1);
+  return cs_tma::launch<CS_BF16, 5120, 3, 20>(items, n_items, h, d_state, s, 1);
 }

@@ -35,6 +35,8 @@ struct Nccl {
                              ncclComm_t, cudaStream_t);
   const char* (*error_string)(ncclResult_t);
   ncclResult_t (*get_version)(int*);
+  ncclResult_t (*get_async_error)(ncclComm_t, ncclResult_t*);
+  ncclResult_t (*comm_abort)(ncclComm_t);
   bool ok = false;
 };
 
@@ -64,6 +66,8 @@ void load_nccl() {
   CS_SYM(all_reduce, "ncclAllReduce")
   CS_SYM(error_string, "ncclGetErrorString")
   CS_SYM(get_version, "ncclGetVersion")
+  CS_SYM(get_async_error, "ncclCommGetAsyncError")
+  CS_SYM(comm_abort, "ncclCommAbort")
 #undef CS_SYM
   int v = 0;
   if (g_nccl.get_version(&v) != ncclSuccess || v < 21000) {  // ncclAvg: NCCL >= 2.10
@@ -179,4 +183,33 @@ extern "C" int cs_allreduce(void* buf, int64_t count, int dtype, int avg, void* 
                                    static_cast<ncclComm_t>(comm),
                                    static_cast<cudaStream_t>(stream)),
                  "cs_allreduce");
+}
+
+// Failure detection: a collective that fails after it was
+// enqueued (a peer died, a network / NVLink error) is reported by NCCL only
+// through the communicator's asynchronous error; the stream it runs on may
+// never complete.  The host polls this (native_comm.py does at every issue
+// and while it waits) and aborts the communicator on error, which unblocks
+// the kernels stuck on it.  Returns 0 while healthy, CS_EINPROGRESS while a
+// nonblocking init / abort is pending, else the ncclResult_t.
+extern "C" int cs_comm_check(void* comm) {
+  if (!comm) {
+    cs::set_error("cs_comm_check: null communicator");
+    return CS_EINVAL;
+  }
+  if (!nccl_ready()) return CS_EUNAVAIL;
+  ncclResult_t async_err = ncclSuccess;
+  if (int rc = nccl_rc(g_nccl.get_async_error(static_cast<ncclComm_t>(comm), &async_err),
+                       "cs_comm_check"))
+    return rc;
+  if (async_err == ncclInProgress) return CS_EINPROGRESS;
+  return nccl_rc(async_err, "cs_comm_check (asynchronous NCCL error)");
+}
+
+// Abort: tear the communicator down without waiting for outstanding
+// collectives (ncclCommAbort); the handle is invalid afterwards.
+extern "C" int cs_comm_abort(void* comm) {
+  if (!comm) return 0;
+  if (!nccl_ready()) return CS_EUNAVAIL;
+  return nccl_rc(g_nccl.comm_abort(static_cast<ncclComm_t>(comm)), "cs_comm_abort");
 }

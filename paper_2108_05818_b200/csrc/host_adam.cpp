@@ -30,88 +30,28 @@ __attribute__((target("avx2,fma,f16c"))) inline __m256 load16(const uint16_t* p)
   return _mm256_castsi256_ps(_mm256_slli_epi32(_mm256_cvtepu16_epi32(h), 16));
 }
 
+// Round-to-nearest-even narrowing; NaN lanes become the canonical NaN
+// 0x7fff, which is what the device conversions (cvt.rn.f16.f32 /
+// cvt.rn.bf16.f32, used by K1) produce -- without the blend a bf16 NaN with
+// high mantissa bits would wrap to -0 and fp16 would keep the payload.
 template <int DT>
 __attribute__((target("avx2,fma,f16c"))) inline void store16(uint16_t* p, __m256 f) {
+  const __m256i nan = _mm256_castps_si256(_mm256_cmp_ps(f, f, _CMP_UNORD_Q));
   __m128i h;
   if (DT == CS_FP16) {
     h = _mm256_cvtps_ph(f, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+    const __m128i nan16 =
+        _mm_packs_epi32(_mm256_castsi256_si128(nan), _mm256_extracti128_si256(nan, 1));
+    h = _mm_blendv_epi8(h, _mm_set1_epi16(0x7fff), nan16);
   } else {  // bf16 round-to-nearest-even: (x + 0x7fff + lsb) >> 16
     const __m256i x = _mm256_castps_si256(f);
     const __m256i lsb = _mm256_and_si256(_mm256_srli_epi32(x, 16), _mm256_set1_epi32(1));
-    const __m256i r = _mm256_srli_epi32(
+    __m256i r = _mm256_srli_epi32(
         _mm256_add_epi32(_mm256_add_epi32(x, _mm256_set1_epi32(0x7fff)), lsb), 16);
+    r = _mm256_blendv_epi8(r, _mm256_set1_epi32(0x7fff), nan);
     h = _mm_packus_epi32(_mm256_castsi256_si128(r), _mm256_extracti128_si256(r, 1));
   }
   _mm_storeu_si128(reinterpret_cast<__m128i*>(p), h);
-}
-
-// in: g16 (gradients), p32, m, v; out: o16, o32, om, ov (may alias the inputs
-// unless STREAM; STREAM needs 32-byte aligned fp32 and 16-byte aligned fp16 outputs)
-template <int DT, bool STREAM = false>
-__attribute__((target("avx2,fma,f16c"))) inline void adam8_oop(
-    const uint16_t* g16, const float* p32, const float* m, const float* v, uint16_t* o16,
-    float* o32, float* om, float* ov, const Consts& c) {
-  __m256 g = _mm256_mul_ps(load16<DT>(g16), c.gs);
-  __m256 p = _mm256_loadu_ps(p32);
-  if (c.has_wd) {
-    if (c.adamw) p = _mm256_mul_ps(p, c.decay);
-    else g = _mm256_fmadd_ps(c.wd, p, g);
-  }
-  const __m256 m0 = _mm256_loadu_ps(m);
-  const __m256 mm = _mm256_fmadd_ps(c.c1, _mm256_sub_ps(g, m0), m0);
-  const __m256 vv = _mm256_fmadd_ps(_mm256_mul_ps(c.c2, g), g,
-                                    _mm256_mul_ps(_mm256_loadu_ps(v), c.b2));
-  const __m256 denom = _mm256_add_ps(_mm256_div_ps(_mm256_sqrt_ps(vv), c.sb), c.eps);
-  p = _mm256_add_ps(p, _mm256_div_ps(_mm256_mul_ps(c.nss, mm), denom));
-  if (STREAM) {  // fresh output lines: non-temporal stores skip the read-for-ownership
-    _mm256_stream_ps(o32, p);
-    _mm256_stream_ps(om, mm);
-    _mm256_stream_ps(ov, vv);
-    alignas(16) uint16_t h[8];
-    store16<DT>(h, p);
-    _mm_stream_si128(reinterpret_cast<__m128i*>(o16),
-                     _mm_load_si128(reinterpret_cast<const __m128i*>(h)));
-  } else {
-    _mm256_storeu_ps(o32, p);
-    _mm256_storeu_ps(om, mm);
-    _mm256_storeu_ps(ov, vv);
-    store16<DT>(o16, p);
-  }
-}
-
-template <int DT>
-__attribute__((target("avx2,fma,f16c"))) void adam_range_oop(const CsAdamItem& in,
-                                                          const CsAdamItem& out, int64_t lo,
-                                                          int64_t hi, const Consts& c) {
-  const uint16_t* g16 = static_cast<const uint16_t*>(in.p16);
-  uint16_t* o16 = static_cast<uint16_t*>(out.p16);
-  int64_t e = lo;
-  const bool aligned = ((reinterpret_cast<uintptr_t>(out.p32) | reinterpret_cast<uintptr_t>(out.m) |
-                         reinterpret_cast<uintptr_t>(out.v)) & 31) == 0 &&
-                       (reinterpret_cast<uintptr_t>(o16) & 15) == 0 && (lo & 7) == 0;
-  if (aligned) {
-    for (; e + 8 <= hi; e += 8)
-      adam8_oop<DT, true>(g16 + e, in.p32 + e, in.m + e, in.v + e, o16 + e, out.p32 + e,
-                          out.m + e, out.v + e, c);
-  } else {
-    for (; e + 8 <= hi; e += 8)
-      adam8_oop<DT>(g16 + e, in.p32 + e, in.m + e, in.v + e, o16 + e, out.p32 + e, out.m + e,
-                    out.v + e, c);
-  }
-  if (e < hi) {  // tail: the same 8-lane code on a padded copy
-    alignas(32) uint16_t t16[8] = {0};
-    alignas(32) float tp[8] = {0}, tm[8] = {0}, tv[8] = {0};
-    const int64_t k = hi - e;
-    std::memcpy(t16, g16 + e, k * 2);
-    std::memcpy(tp, in.p32 + e, k * 4);
-    std::memcpy(tm, in.m + e, k * 4);
-    std::memcpy(tv, in.v + e, k * 4);
-    adam8_oop<DT>(t16, tp, tm, tv, t16, tp, tm, tv, c);
-    std::memcpy(o16 + e, t16, k * 2);
-    std::memcpy(out.p32 + e, tp, k * 4);
-    std::memcpy(out.m + e, tm, k * 4);
-    std::memcpy(out.v + e, tv, k * 4);
-  }
 }
 
 template <int DT>
@@ -208,7 +148,7 @@ extern "C" int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dty
     return CS_EINVAL;
   }
   if (state->skip) {  // non-finite gradients: no update, p16 = round(p32) restored
-    const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+    const int threads = cs::host_threads(n_threads);
     for (int i = 0; i < n_items; ++i)
       if (dtype == CS_FP16) restore_item<CS_FP16>(items[i], threads);
       else restore_item<CS_BF16>(items[i], threads);
@@ -226,7 +166,7 @@ extern "C" int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dty
     for (int64_t lo = 0; lo < items[i].n; lo += kRange) ranges.emplace_back(i, lo);
   }
   const int64_t nr = (int64_t)ranges.size();
-  const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+  const int threads = cs::host_threads(n_threads);
 #pragma omp parallel for num_threads(threads) schedule(static)
   for (int64_t r = 0; r < nr; ++r) {
     const CsAdamItem& it = items[ranges[r].first];
@@ -234,49 +174,6 @@ extern "C" int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dty
     const int64_t hi = lo + kRange < it.n ? lo + kRange : it.n;
     if (dtype == CS_FP16) adam_range<CS_FP16>(it, lo, hi, c);
     else adam_range<CS_BF16>(it, lo, hi, c);
-  }
-  return 0;
-}
-
-extern "C" int cs_adam_chunks_host_oop(const CsAdamItem* in, const CsAdamItem* out,
-                                       int n_items, int dtype, const CsAdamHyper* hyper,
-                                       const CsStepState* state, int n_threads) {
-  if (n_items < 0 || (n_items > 0 && (!in || !out)) || !hyper || !state ||
-      (dtype != CS_FP16 && dtype != CS_BF16) || state->skip) {
-    cs::set_error("cs_adam_chunks_host_oop: invalid argument (a skipped step has no update)");
-    return CS_EINVAL;
-  }
-  if (!__builtin_cpu_supports("avx2") || !__builtin_cpu_supports("fma") ||
-      !__builtin_cpu_supports("f16c")) {
-    cs::set_error("cs_adam_chunks_host_oop: host CPU lacks AVX2/FMA/F16C");
-    return CS_EINVAL;
-  }
-  const Consts c = make_consts(*hyper, *state);
-  constexpr int64_t kRange = 1 << 16;
-  std::vector<std::pair<int, int64_t>> ranges;
-  for (int i = 0; i < n_items; ++i) {
-    const CsAdamItem& a = in[i];
-    const CsAdamItem& b = out[i];
-    if (a.n < 0 || a.n != b.n ||
-        (a.n > 0 && (!a.p16 || !a.p32 || !a.m || !a.v || !b.p16 || !b.p32 || !b.m || !b.v))) {
-      cs::set_error("cs_adam_chunks_host_oop: item %d invalid", i);
-      return CS_EINVAL;
-    }
-    for (int64_t lo = 0; lo < a.n; lo += kRange) ranges.emplace_back(i, lo);
-  }
-  const int64_t nr = (int64_t)ranges.size();
-  const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
-#pragma omp parallel num_threads(threads)
-  {
-#pragma omp for schedule(static)
-    for (int64_t r = 0; r < nr; ++r) {
-      const int i = ranges[r].first;
-      const int64_t lo = ranges[r].second;
-      const int64_t hi = lo + kRange < in[i].n ? lo + kRange : in[i].n;
-      if (dtype == CS_FP16) adam_range_oop<CS_FP16>(in[i], out[i], lo, hi, c);
-      else adam_range_oop<CS_BF16>(in[i], out[i], lo, hi, c);
-    }
-    _mm_sfence();  // each thread's non-temporal stores are visible before the join
   }
   return 0;
 }
@@ -311,7 +208,7 @@ extern "C" int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtyp
     cs::set_error("cs_grad_sumsq_host: host CPU lacks AVX2/F16C");
     return CS_EINVAL;
   }
-  const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+  const int threads = cs::host_threads(n_threads);
   double total = 0.0;
   for (int i = 0; i < n_items; ++i) {
     const uint16_t* g = static_cast<const uint16_t*>(items[i].g16);

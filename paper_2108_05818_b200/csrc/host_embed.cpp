@@ -162,7 +162,7 @@ extern "C" int cs_embed_fwd_host(const int64_t* tokens, int64_t n_tokens, int se
     return CS_EINVAL;
   }
   if (int rc = check_tokens(tokens, n_tokens, vocab, "cs_embed_fwd_host")) return rc;
-  const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+  const int threads = cs::host_threads(n_threads);
   const auto* a = static_cast<const uint16_t*>(wte);
   const auto* b = static_cast<const uint16_t*>(wpe);
   auto* o = static_cast<uint16_t*>(out);
@@ -186,7 +186,7 @@ extern "C" int cs_embed_bwd_host(const int64_t* tokens, int64_t n_tokens, int se
     return CS_EINVAL;
   }
   if (int rc = check_tokens(tokens, n_tokens, vocab, "cs_embed_bwd_host")) return rc;
-  const int threads = n_threads > 0 ? n_threads : omp_get_max_threads();
+  const int threads = cs::host_threads(n_threads);
   const auto* d = static_cast<const uint16_t*>(dout);
   auto* gw = static_cast<uint16_t*>(gwte);
   auto* gp = static_cast<uint16_t*>(gwpe);

@@ -179,12 +179,17 @@ int run_pack(const char* what, const CsPackItem* items, int n_items, int dtype, 
     cs::set_error("%s: invalid argument", what);
     return CS_EINVAL;
   }
+  if (n_items > CS_MAX_ITEMS) {
+    cs::set_error("%s: %d items > CS_MAX_ITEMS", what, n_items);
+    return CS_ETOOMANY;
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int first = 0; first < n_items; first += cs::kMaxBatch) {
+  for (int first = 0; first < n_items;) {
     PackBatch b;
     b.count = 0;
     int64_t tiles = 0;
-    for (int i = first; i < n_items && b.count < cs::kMaxBatch; ++i) {
+    int i = first;
+    for (; i < n_items && b.count < cs::kMaxBatch; ++i) {
       const CsPackItem& it = items[i];
       if (it.n < 0 || it.offset < 0 || (it.n > 0 && (!it.chunk || !it.src))) {
         cs::set_error("%s: item %d invalid", what, i);
@@ -200,6 +205,7 @@ int run_pack(const char* what, const CsPackItem* items, int n_items, int dtype, 
       tiles += (it.n + kBlockTile - 1) / kBlockTile;
       ++b.count;
     }
+    first = i;  // resume where this batch stopped (zero-length items took no slot)
     b.tile_start[b.count] = tiles;
     if (b.count == 0) continue;
     const int grid = grid_for(tiles);

@@ -113,6 +113,7 @@ class _IterState:
     coll_bytes_before: int
     next_event: int = 0
     failed: bool = False
+    moment: int = 0
 
 
 class Engine:
@@ -142,6 +143,10 @@ class Engine:
         self.non_model_fn = non_model_fn
         self.embedding_device = CPU
         self.measured_strategy = manager.strategy
+        #: physical allocation failures raised inside the executor hooks
+        #: (e.g. torch.OutOfMemoryError) become GPU_OOM like the accounting's
+        #: OOMError (`engine.py:349-352` of the reference); set by the trainer
+        self.physical_oom: tuple = ()
         self.warmup_stats: Optional[WarmupStats] = None
         self.plan: Optional[PlacementPlan] = None
         self._computing: Dict[int, Chunk] = {}  # chunks holding COMPUTE tensors
@@ -386,10 +391,21 @@ class Engine:
         try:
             fn()
         except OOMError as oom:
-            it.failed = True
-            it.report.feasible = False
-            it.report.failure_reason = "GPU_OOM" if oom.device == GPU else "CPU_OOM"
-            it.report.failure_moment = oom.moment
+            self.fail_iteration(oom.device, oom.moment)
+        except self.physical_oom:
+            self.fail_iteration(GPU, it.moment)
+
+    def fail_iteration(self, device: str, moment: Optional[int] = None) -> None:
+        """Mark the open iteration infeasible (the reference's OOM verdict,
+        `engine.py:349-352`); its remaining events are skipped and
+        :meth:`end_iteration` returns the infeasible report."""
+        it = self._it
+        if it is None or it.failed:
+            return
+        it.failed = True
+        it.report.feasible = False
+        it.report.failure_reason = "GPU_OOM" if device == GPU else "CPU_OOM"
+        it.report.failure_moment = it.moment if moment is None else moment
 
     def start_event(self, ev) -> None:
         """Rising edge of event ``ev`` plus the during-event sample."""
@@ -401,9 +417,10 @@ class Engine:
 
     def _start_body(self, ev) -> None:
         it = self._it
+        m = 2 * ev.index + 1
+        it.moment = m
         if self.executor is not None:
             self.executor.before_event(ev, it.report.iteration)
-        m = 2 * ev.index + 1
         self.manager.set_non_model(GPU, self.non_model_fn(m), m)
         if ev.phase is Phase.ADAM:
             if it.plan_builder is not None:
@@ -425,6 +442,7 @@ class Engine:
 
     def _finish_body(self, ev) -> None:
         m = 2 * ev.index + 1
+        self._it.moment = m
         if ev.kind is OpKind.EMBEDDING:
             self._embedding_finish(ev)
         elif ev.phase is not Phase.ADAM:

@@ -25,17 +25,28 @@ from . import _native as N
 CODE = {torch.float16: N.CS_FP16, torch.bfloat16: N.CS_BF16, torch.float32: N.CS_FP32}
 
 
-class _Work:
-    __slots__ = ("_event",)
+class NcclAsyncError(RuntimeError):
+    """A collective failed after it was enqueued (ncclCommGetAsyncError);
+    the communicator has been aborted."""
 
-    def __init__(self, event: torch.cuda.Event):
+
+class _Work:
+    __slots__ = ("_event", "_comm")
+
+    def __init__(self, event: torch.cuda.Event, comm: "NativeChunkComm"):
         self._event = event
+        self._comm = comm
 
     def wait(self) -> None:
         torch.cuda.current_stream().wait_event(self._event)
 
     def is_completed(self) -> bool:
         return self._event.query()
+
+    def wait_host(self, timeout_s: float = 600.0) -> None:
+        """Block the host until the collective completed, polling the
+        communicator's asynchronous error; abort it on error or timeout."""
+        self._comm.wait_event_host(self._event, timeout_s)
 
 
 class NativeChunkComm:
@@ -63,6 +74,38 @@ class NativeChunkComm:
                     "cs_comm_init")
         self.stream = torch.cuda.Stream(self.device)
 
+    def check(self) -> None:
+        """Raise (after aborting the communicator) if a collective failed
+        asynchronously; SURVEY §5 failure detection."""
+        if not self._comm:
+            raise NcclAsyncError("the communicator was aborted")
+        rc = N.load().cs_comm_check(self._comm)
+        if rc not in (0, N.CS_EINPROGRESS):
+            msg = N.load().cs_last_error().decode(errors="replace")
+            self.abort()
+            raise NcclAsyncError("NCCL asynchronous error (rc=%d): %s" % (rc, msg))
+
+    def abort(self) -> None:
+        """ncclCommAbort: unblocks kernels stuck on a dead peer; the
+        communicator cannot be used afterwards."""
+        if self._comm:
+            N.load().cs_comm_abort(self._comm)
+            self._comm = ctypes.c_void_p()
+
+    def wait_event_host(self, event: torch.cuda.Event, timeout_s: float = 600.0) -> None:
+        import time
+        t0 = time.monotonic()
+        delay = 1e-4
+        while not event.query():
+            self.check()
+            if time.monotonic() - t0 > timeout_s:
+                self.abort()
+                raise NcclAsyncError("collective did not complete in %.0f s; communicator "
+                                     "aborted" % timeout_s)
+            time.sleep(delay)
+            delay = min(delay * 2, 0.05)
+        self.check()
+
     def close(self) -> None:
         if self._comm:
             N.check(N.load().cs_comm_destroy(self._comm), "cs_comm_destroy")
@@ -79,6 +122,7 @@ class NativeChunkComm:
             pass
 
     def _run(self, call, async_op: bool, *tensors: torch.Tensor):
+        self.check()  # a failed earlier collective surfaces at the next issue
         cur = torch.cuda.current_stream(self.device)
         self.stream.wait_stream(cur)
         for t in tensors:  # the caching allocator must not recycle them under the op
@@ -86,7 +130,7 @@ class NativeChunkComm:
         call(ctypes.c_void_p(self.stream.cuda_stream))
         ev = torch.cuda.Event()
         ev.record(self.stream)
-        work = _Work(ev)
+        work = _Work(ev, self)
         if async_op:
             return work
         work.wait()

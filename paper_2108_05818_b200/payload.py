@@ -87,6 +87,13 @@ class ChunkComm:
     def all_reduce_sum(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
+    def check(self) -> None:
+        """Failure detection: torch's NCCL process group surfaces
+        asynchronous collective errors from its own watchdog (it aborts the
+        communicator and raises at the next call), so there is nothing to
+        poll here; :class:`.native_comm.NativeChunkComm` polls
+        ncclCommGetAsyncError itself."""
+
     def all_reduce_avg(self, t: torch.Tensor) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.AVG, group=self.group)
 
@@ -118,12 +125,10 @@ class ExecStats:
     prefetch_hits: int = 0
     prefetch_discarded: int = 0
     prefetch_discarded_bytes: int = 0
+    early_drains: int = 0
     gather_prefetch_issued: int = 0
     gather_prefetch_hits: int = 0
     host_adam_seconds: float = 0.0
-    spec_issued: int = 0
-    spec_committed: int = 0
-    spec_discarded: int = 0
     copy_events: List[Tuple[str, int, "torch.cuda.Event", "torch.cuda.Event"]] = field(
         default_factory=list)
 
@@ -186,32 +191,15 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.async_host_adam = os.environ.get("CS_ASYNC_HOST_ADAM", "1") != "0"
         self._worker: Optional[ThreadPoolExecutor] = None
         self._jobs: Dict[int, _HostAdamJob] = {}   # chunk id -> unfinished job
-        #: speculative host Adam (CS_SPEC_HOST_ADAM=1): a host-placed position's
-        #: gradients are drained D2H as soon as its last BWD op is enqueued and
-        #: its update runs on the worker during the rest of the backward, out
-        #: of place into shadow buffers, with the scalars cs_adam_prepare will
-        #: produce if the step is finite and unclipped.  At the position's ADAM
-        #: turn the shadows become the payloads (pointer swap) when the real
-        #: scalars match bit for bit; otherwise they are dropped and the normal
-        #: update runs.  Single rank only (at p > 1 the reduce-scatter comes first).
-        #: Off by default: bit-identical (tests), but measured SLOWER on the
-        #: 16-core B200 hosts — 1B with every triplet on the host 361-407 vs
-        #: 353-354 ms/step, 12B mixed 2.30 vs 2.04 s
-        #: (profiles/r01/speculative_host_adam_ab.txt) — because the async host
-        #: Adam already overlaps the next forward, and an update running beside
-        #: the backward's enqueue and D2Hs streams at 4.4-4.6 instead of 5.3
-        #: Gelem/s even with non-temporal stores into the shadows.
-        self.speculative_host_adam = os.environ.get("CS_SPEC_HOST_ADAM", "0") == "1"
-        self.spec_max_positions = int(os.environ.get("CS_SPEC_MAX_POSITIONS", "64"))
-        # OpenMP threads of a speculative update (0: all cores; fewer measured
-        # slower: 1B all-host step 478 / 412 / 389-404 ms at 8 / 12 / 16)
-        self.spec_threads = int(os.environ.get("CS_SPEC_THREADS", "0")) or host_threads
-        self._timeline = None
-        self._last_bwd: Optional[Dict[int, int]] = None   # position -> last BWD event
-        self._spec: Dict[int, tuple] = {}        # position -> (future, d, ins, shadow)
-        self._spec_free: List[tuple] = []        # recycled (p16, p32, m, v) host buffers
-        self._spec_seen: Set[int] = set()
-        self._spec_state = None
+        #: drain a host-placed position's gradients D2H as soon as they are
+        #: final (after its last BWD op; at p > 1 after its reduce-scatter),
+        #: during the backward while host DRAM is otherwise idle, instead of at
+        #: ADAM beside the host Adam; the accounting still bills the row at the
+        #: position's ADAM turn (`engine.py:249-251`), where the copy is adopted
+        self.early_drain = os.environ.get("CS_EARLY_DRAIN", "1") != "0"
+        self._last_bwd_at: Optional[Dict[int, List[int]]] = None  # event -> positions
+        self._drain_candidates: List[int] = []
+        self._rs_out: Set[int] = set()  # local chunks whose reduce-scatter was issued
         self._stats_lock = threading.Lock()
         #: CPU-placed embedding operator (embedding.HostEmbedding) or None
         self.host_embedding = None
@@ -402,19 +390,23 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     self.ready[(cid, GPU)] = done
 
     def _transfer(self, s: torch.Tensor, d: torch.Tensor, src: str, dst: str,
-                  prior: Optional["torch.cuda.Event"]):
+                  prior: Optional["torch.cuda.Event"], after=None):
         """cudaMemcpyAsync of a whole payload on the copy stream of its
         direction; returns the completion event consumers wait on
         (`wait_ready`).  D2H waits for the compute stream (the payload must be
         final); H2D does not (its source is host data already final, its
         destination came from the H2D stream's pool).  A move that depends on
-        an earlier one (a fetch of a chunk just evicted) waits on its event."""
+        an earlier one (a fetch of a chunk just evicted) waits on its event;
+        ``after``: a collective Work still writing the source (a D2H of
+        reduce-scattered gradients waits for it on the copy stream only)."""
         cs = self.d2h_stream if src == GPU else self.copy_stream
         if src == GPU:
             cs.wait_stream(self.compute)
         if prior is not None:
             cs.wait_event(prior)
         with torch.cuda.stream(cs):
+            if after is not None:
+                after.wait()
             t0 = torch.cuda.Event(enable_timing=True) if self.time_copies else None
             if t0 is not None:
                 t0.record(cs)
@@ -457,13 +449,50 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._prefetch_sched = sched
 
     def set_timeline(self, timeline) -> None:
-        self._timeline = timeline
-        self._last_bwd = None
+        """Index the positions by their last BWD event (early gradient drain)."""
+        last: Dict[int, int] = {}
+        for e in timeline.events:
+            if e.phase.value == "bwd":
+                for tid in e.tensor_refs:
+                    pos = self.offsets[tid][0]
+                    last[pos] = max(last.get(pos, -1), e.index)
+        by_event: Dict[int, List[int]] = {}
+        for pos, e in last.items():
+            by_event.setdefault(e, []).append(pos)
+        self._last_bwd_at = by_event
+
+    def _drain_early(self, ev) -> None:
+        """D2H of host-placed positions' final gradients, ahead of ADAM."""
+        if self._plan is None or self._last_bwd_at is None or ev.phase.value == "adam":
+            return
+        local = set(self.partition.local_positions(self.rank))
+        for pos in self._last_bwd_at.get(ev.index - 1, ()):
+            if pos in local and self._plan.device_of_position(pos) == CPU:
+                self._drain_candidates.append(pos)
+        if not self._drain_candidates:
+            return
+        multi = self.comm is not None and self.comm.world > 1
+        keep = []
+        for pos in self._drain_candidates:
+            chunk = self.chunk_set.param_chunk(pos)
+            cid = chunk.chunk_id
+            if multi and cid not in self._rs_out:
+                keep.append(pos)  # its group's reduce-scatter is not issued yet
+                continue
+            if not self.has(chunk, GPU) or self.has(chunk, CPU) or cid in self._predrained \
+                    or cid in self._awaiting_gather:
+                continue
+            d = self._alloc(chunk, CPU)
+            done = self._transfer(self.tensor(chunk, GPU), d, GPU, CPU,
+                                  self.ready.get((cid, GPU)), after=self._coll_work.get(cid))
+            self._predrained[cid] = (d, done)
+            self.stats.early_drains += 1
+        self._drain_candidates = keep
 
     def before_event(self, ev, iteration: int) -> None:
         self._cur_event = ev.index
-        if self.speculative_host_adam and self._timeline is not None:
-            self._speculate(ev.index)
+        if self.early_drain:
+            self._drain_early(ev)
         if self.comm is not None and self.comm.world > 1:
             self._prefetch_gathers(ev)
         if not self.prefetch_depth or not self._prefetch_sched:
@@ -482,85 +511,6 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 done = self._transfer(src, d, CPU, GPU, prior)
                 self._prefetched[cid] = (d, done)
                 self.stats.prefetch_issued += 1
-
-    def _speculate(self, event_index: int) -> None:
-        """Start the speculative host Adam of every host-placed position whose
-        last BWD op precedes ``event_index`` (see ``speculative_host_adam``)."""
-        plan = self._plan
-        if (plan is None or self._state_snap is None or not self.async_host_adam
-                or (self.comm is not None and self.comm.world > 1)):
-            return
-        cs = self.chunk_set
-        if self._last_bwd is None:
-            last: Dict[int, int] = {}
-            for e in self._timeline.events:
-                if e.phase.value == "bwd":
-                    for tid in e.tensor_refs:
-                        pos = self.offsets[tid][0]
-                        last[pos] = max(last.get(pos, -1), e.index)
-            self._last_bwd = last
-        for pos, last_ev in self._last_bwd.items():
-            if last_ev >= event_index or pos in self._spec_seen:
-                continue
-            self._spec_seen.add(pos)
-            if plan.device_of_position(pos) != CPU or len(self._spec) >= self.spec_max_positions:
-                continue
-            chunk = cs.param_chunk(pos)
-            cid = chunk.chunk_id
-            triplet = cs.os_triplet(pos)
-            if (not self.has(chunk, GPU) or self.has(chunk, CPU) or cid in self._predrained
-                    or cid in self._jobs or cid in self._awaiting_gather
-                    or any(not self.has(c, CPU) or c.chunk_id in self._jobs for c in triplet)):
-                continue
-            if self._spec_state is None:
-                self._spec_state = K.speculate_step_scalars(
-                    K.StepState.from_snapshot(self._state_snap), self.hyper)
-            d = self._alloc(chunk, CPU)
-            done = self._transfer(self.tensor(chunk, GPU), d, GPU, CPU,
-                                  self.ready.get((cid, GPU)))
-            self._predrained[cid] = (d, done)
-            shadow = (self._spec_free.pop() if self._spec_free else
-                      tuple(self._alloc(c, CPU) for c in (chunk,) + triplet))
-            n = chunk.used_elems
-            ins = (d,) + tuple(self.tensor(c, CPU) for c in triplet)
-            waits = [done] + [self.ready[(c.chunk_id, CPU)] for c in triplet
-                              if (c.chunk_id, CPU) in self.ready]
-            if self._worker is None:
-                self._worker = ThreadPoolExecutor(max_workers=1,
-                                                  thread_name_prefix="cs-host-adam")
-            fut = self._worker.submit(self._run_spec, waits, ins + (n,), shadow + (n,),
-                                      self._spec_state)
-            self._spec[pos] = (fut, d, ins, shadow)
-            self.stats.spec_issued += 1
-
-    def _run_spec(self, waits, item_in, item_out, state) -> None:
-        for ev in waits:
-            ev.synchronize()
-        t0 = time.perf_counter()
-        K.adam_chunks_host_oop([item_in], [item_out], self.hyper, state, self.spec_threads)
-        with self._stats_lock:
-            self.stats.host_adam_seconds += time.perf_counter() - t0
-
-    def _commit_spec(self, position: int, param: Chunk, triplet) -> bool:
-        """At the position's ADAM turn: adopt its speculative update if the
-        real step scalars are the speculated ones and the payloads are the
-        buffers it read; else recycle the shadows.  True when committed."""
-        fut, d, ins, shadow = self._spec.pop(position)
-        fut.result()
-        cpu = self.payload[CPU]
-        ok = (K.same_update_scalars(self._spec_state, self._host_state)
-              and cpu.get(param.chunk_id) is d
-              and all(cpu.get(c.chunk_id) is t for c, t in zip(triplet, ins[1:])))
-        if not ok:
-            self._spec_free.append(shadow)
-            self.stats.spec_discarded += 1
-            return False
-        for c, t in zip((param,) + tuple(triplet), shadow):
-            cpu[c.chunk_id] = t
-        self._spec_free.append(ins)
-        self.stats.spec_committed += 1
-        self.stats.host_adam_items += 1
-        return True
 
     def _discard_prefetch(self, chunk: Chunk) -> None:
         hit = self._prefetched.pop(chunk.chunk_id, None)
@@ -700,6 +650,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self._inflight.append((work, (slab, out)))
             if out_cid is not None:
                 self._coll_work[out_cid] = work
+        if out_cid is not None:
+            self._rs_out.add(out_cid)
         self._group_slab[group.group_id] = slab
         self.stats.reduce_scatters += 1
 
@@ -732,6 +684,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def on_adam_begin(self, iteration: int, plan=None) -> None:
         """Global grad norm / found-inf and the device step scalars."""
+        if self.comm is not None and hasattr(self.comm, "check"):
+            self.comm.check()  # a collective of this step failed asynchronously
         self.join_host_work()  # the previous step's host updates are complete
         cs = self.chunk_set
         self._plan = plan
@@ -843,8 +797,6 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self._host_state = self._step_scalars_on_host()
         for c in (param,) + triplet:
             self.wait_ready(c, CPU)
-        if position in self._spec and self._commit_spec(position, param, triplet):
-            return
         p16 = self.tensor(param, CPU)
         p32, m, v = (self.tensor(c, CPU) for c in triplet)
         item = (p16, p32, m, v, n)
@@ -907,13 +859,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 self.stats.host_adam_seconds += dt
             he.host_seconds += dt
             he.grads_ready = False
-        for pos in list(self._spec):  # never reached its ADAM turn: recycle
-            fut, _, _, shadow = self._spec.pop(pos)
-            fut.result()
-            self._spec_free.append(shadow)
-            self.stats.spec_discarded += 1
-        self._spec_seen.clear()
-        self._spec_state = None
+        self._drain_candidates = []
+        self._rs_out.clear()
         self._retain_req.clear()
         for (cid, dev), t in self._retained.items():
             if dev == GPU:

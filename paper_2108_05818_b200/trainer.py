@@ -22,7 +22,8 @@ records the access trace; the placement plan is computed at its ADAM event
 import gc
 import os
 import time
-from typing import Callable, List, Optional
+import warnings
+from typing import Callable, Dict, List, Optional
 
 import torch
 
@@ -35,7 +36,9 @@ from .memory import OOMError
 from .model import CPU, GPU, ModelSchema
 from .embedding import HostEmbedding
 from .payload import ChunkComm, ChunkPayloadExecutor
+from .profiler import embedding_compute_device
 from .scenario import Simulator
+from . import hostres
 
 
 def _host_ram_bytes() -> int:
@@ -64,6 +67,25 @@ class PendingLoss:
         return float(self._host)
 
 
+class StepInfeasible(OOMError):
+    """A training step ran out of memory: the accounting's OOMError, or a
+    physical allocation failure (torch.OutOfMemoryError) — the reference
+    turns both into an infeasible IterationReport (`engine.py:349-352`),
+    which is ``.report`` (also the trainer's last report).  The trainer
+    refuses further steps: like the reference's ``Simulator.run``
+    (`scenario.py:176-181`), a run stops at its first infeasible iteration."""
+
+    def __init__(self, report: IterationReport, cause: Optional[BaseException] = None):
+        dev = "gpu" if report.failure_reason == "GPU_OOM" else "cpu"
+        moment = -1 if report.failure_moment is None else report.failure_moment
+        super().__init__(dev, moment, 0, 0)
+        self.args = ("iteration %d infeasible: %s at moment %d%s"
+                     % (report.iteration, report.failure_reason, moment,
+                        "" if cause is None else " (%s)" % str(cause).splitlines()[0][:200]),)
+        self.report = report
+        self.cause = cause
+
+
 class ChunkTrainer:
     """Chunk-managed (PatrickStar) data-parallel GPT training on one GPU per rank."""
 
@@ -77,11 +99,11 @@ class ChunkTrainer:
                  non_model_fn: Optional[Callable[[int], int]] = None,
                  host_threads: int = 0, time_copies: bool = False,
                  cuda_graph: bool = False, fused_ops: bool = True,
-                 prefetch_depth: int = 2, non_model: str = "analytic",
+                 prefetch_depth: int = 2, non_model: str = "auto",
                  gather_depth: int = 2, embedding_placement: str = "plan",
-                 untied_head: Optional[bool] = None,
+                 untied_head: bool = False,
                  async_host_adam: Optional[bool] = None,
-                 comm=None, speculative_host_adam: Optional[bool] = None):
+                 comm=None, bind_host: Optional[bool] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -100,14 +122,57 @@ class ChunkTrainer:
             else:
                 comm = ChunkComm(process_group)
             nproc, rank = comm.world, comm.rank
+        # host cores: one process per GPU binds to its share of its GPU's NUMA
+        # node (pinned slabs are first-touched there too) and every host
+        # kernel gets an explicit team size (torchrun sets OMP_NUM_THREADS=1)
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        if bind_host is None:
+            bind_host = local_world > 1
+        self.host_binding = (hostres.bind_local_rank(
+            int(os.environ.get("LOCAL_RANK", "0")), local_world, self.device.index or 0)
+            if bind_host else {"bound": False})
+        host_threads = hostres.host_threads(host_threads)
+        self.host_threads = host_threads
+        # where the embedding operator physically runs: the reference's plan
+        # (`profiler.py:70-74`, the Simulator sets it on the engine) unless
+        # forced.  A CPU-placed embedding needs an untied LM head (the tied
+        # head's weights are the embedding's, needed on the GPU from the first
+        # forward op to the last backward op), and the untied head is an
+        # explicit opt-in: the batch size must not change the model.  So a
+        # tied model whose plan says CPU computes the embedding on the GPU.
+        planned_emb = embedding_compute_device(schema)
+        if embedding_placement == "plan":
+            embedding_placement = planned_emb
+            if planned_emb == CPU and not untied_head:
+                warnings.warn("the placement plan puts the embedding on the CPU, which needs "
+                              "an untied LM head (untied_head=True); this tied model computes "
+                              "it on the GPU and the ledger's embedding rows are not realized",
+                              stacklevel=2)
+                embedding_placement = GPU
+        if embedding_placement not in (CPU, GPU):
+            raise ValueError("embedding_placement must be 'plan', 'cpu' or 'gpu'")
+        if embedding_placement == CPU and not untied_head:
+            raise ValueError("a CPU-placed embedding needs an untied LM head (untied_head=True)")
+        V, H, S = schema.vocab, schema.hidden_dim, schema.seq_len
+        # non-chunked parameters that live in HBM for the whole run: fp16/bf16
+        # weights (their gradients overwrite them) + fp32 master / m / v
+        gpu_resident_elems = (0 if embedding_placement == CPU else (V + S) * H) + \
+            (V * H if untied_head else 0)
+        self.gpu_resident_bytes = gpu_resident_elems * (2 + 12)
+        if non_model == "auto":
+            non_model = "measured" if hardware is None and non_model_fn is None else "analytic"
         if hardware is None:
             total = torch.cuda.get_device_properties(self.device).total_memory
-            # the accounting may plan chunks into 90 % of HBM; the rest is the
-            # CUDA context, library workspaces, NCCL buffers and allocator slack.
-            # (0.85 removes the last allocator retries of the 12B mixed-placement
-            # step, 2.3 vs 2.3-3.0 s, but costs the 12B checkpointed step 47 GB
-            # of chunk moves per step instead of 6 GB: 1.38 vs 0.83 s.)
-            hardware = HardwareSpec(gpu_count=nproc, gpu_bytes=int(total * 0.9),
+            # the accounting may plan chunks into a fraction of HBM minus the
+            # non-chunked state resident beside them (charged here so the
+            # planner never commits HBM that is already in use); the rest is
+            # the CUDA context, NCCL buffers and allocator slack.  With the
+            # measured warm-up tracer R - C already holds the activations and
+            # library workspaces, so less slack is kept than with the
+            # reference's analytic activation model.
+            frac = 0.93 if non_model == "measured" else 0.9
+            hardware = HardwareSpec(gpu_count=nproc,
+                                    gpu_bytes=int(total * frac) - self.gpu_resident_bytes,
                                     cpu_bytes=int(_host_ram_bytes() * 0.8))
         fp16 = dtype == torch.float16
         if dynamic_loss_scale is None:
@@ -122,8 +187,6 @@ class ChunkTrainer:
         ex = self.executor
         if async_host_adam is not None:
             ex.async_host_adam = async_host_adam
-        if speculative_host_adam is not None:
-            ex.speculative_host_adam = speculative_host_adam
         self.tracer = None
         if non_model == "measured" and non_model_fn is None:
             from .tracer import MemoryTracer
@@ -134,19 +197,10 @@ class ChunkTrainer:
                              payload_backend=ex, collective_backend=ex, executor=ex,
                              non_model_fn=non_model_fn)
         self.nproc, self.rank = nproc, rank
-        ex.set_timeline(self.sim.timeline)
-        # where the embedding operator physically runs: the reference's plan
-        # (`profiler.py:70-74`, set on the engine by the Simulator) unless forced
-        if embedding_placement == "plan":
-            embedding_placement = self.sim.engine.embedding_device
-        if embedding_placement not in (CPU, GPU):
-            raise ValueError("embedding_placement must be 'plan', 'cpu' or 'gpu'")
+        assert self.sim.engine.embedding_device == planned_emb
         self.embedding_placement = embedding_placement
+        self.untied_head = untied_head
         host_emb = embedding_placement == CPU
-        if untied_head is None:
-            untied_head = host_emb
-        if host_emb and not untied_head:
-            raise ValueError("a CPU-placed embedding needs an untied LM head")
         with torch.device(self.device):
             self.model = ReferenceShapedGPT(schema, dtype=dtype, placeholders=True,
                                             fused=fused_ops, untied_head=untied_head)
@@ -179,9 +233,12 @@ class ChunkTrainer:
         ex.attach(self.sim.chunk_set, self.sim.partition, rank,
                   self.model.chunk_parameters(), self.shapes,
                   [(p, mst.view(-1), m.view(-1), v.view(-1)) for p, mst, m, v in emb])
+        ex.set_timeline(self.sim.timeline)
         self._init_weights(seed, emb)
         self.iteration = 0
         self.reports: List[IterationReport] = []
+        self.failed: Optional[IterationReport] = None
+        self.sim.engine.physical_oom = (torch.OutOfMemoryError,)
         self.cuda_graph = cuda_graph
         self.prefetch_depth = prefetch_depth
         self.gather_depth = gather_depth
@@ -244,9 +301,22 @@ class ChunkTrainer:
 
     def _check(self) -> None:
         if self.sim.engine.iteration_failed:
-            r = self.sim.engine._it.report
-            raise OOMError("gpu" if r.failure_reason == "GPU_OOM" else "cpu",
-                           -1 if r.failure_moment is None else r.failure_moment, 0, 0)
+            raise StepInfeasible(self._end_failed())
+
+    def _end_failed(self, cause: Optional[BaseException] = None) -> IterationReport:
+        """Close an infeasible iteration: its report is recorded, the
+        host-side work it started is joined, the trainer is marked failed."""
+        eng = self.sim.engine
+        if cause is not None:
+            eng.fail_iteration(GPU)
+        try:
+            self.executor.join_host_work()
+        except Exception:
+            pass
+        report = eng.end_iteration()
+        self.reports.append(report)
+        self.failed = report
+        return report
 
     def _on_start(self, idx: int) -> None:
         self.sim.engine.start_event(self._events[idx])
@@ -278,22 +348,30 @@ class ChunkTrainer:
         return self._eager_step(tokens)
 
     def _eager_step(self, tokens: torch.Tensor) -> torch.Tensor:
+        if self.failed is not None:
+            raise RuntimeError("iteration %d was infeasible (%s); this run cannot continue"
+                               % (self.failed.iteration, self.failed.failure_reason))
         eng = self.sim.engine
         warm = self.iteration == 0
         eng.begin_iteration(self.iteration, warm,
                             self.sim._plan_builder() if warm else None, self.sim.local)
         self._check()
-        t0 = time.perf_counter()
-        inp, tgt = tokens[:, :-1], tokens[:, 1:]
-        loss = self.model(inp, tgt)
-        t1 = time.perf_counter()
-        (loss * self.executor.state.loss_scale()).backward()
-        t2 = time.perf_counter()
-        adam = self._events[-1]
-        eng.start_event(adam)
-        self._check()
-        eng.finish_event(adam)
-        self._check()
+        try:
+            t0 = time.perf_counter()
+            inp, tgt = tokens[:, :-1], tokens[:, 1:]
+            loss = self.model(inp, tgt)
+            t1 = time.perf_counter()
+            (loss * self.executor.state.loss_scale()).backward()
+            t2 = time.perf_counter()
+            adam = self._events[-1]
+            eng.start_event(adam)
+            self._check()
+            eng.finish_event(adam)
+            self._check()
+        except torch.OutOfMemoryError as e:
+            # a physical allocation failed outside the engine's hooks (the
+            # model's activations): the same verdict at the current moment
+            raise StepInfeasible(self._end_failed(e), e) from None
         ph = self.phase_seconds  # host time per phase (enqueue + any blocking waits)
         ph["fwd"] += t1 - t0
         ph["bwd"] += t2 - t1
@@ -438,6 +516,23 @@ class ChunkTrainer:
         from . import ledgers
         return ledgers.write_ledgers(out_dir, self.reports, self.sim.chunk_set.layout_rows(),
                                      self.sim.engine.plan)
+
+    def ledger_rows_not_realized(self, report: Optional[IterationReport] = None) -> Dict[str, int]:
+        """Bytes per step the ledger bills that this run does not physically
+        move.  Only the embedding's rows can be: the reference bills a
+        GPU-placed embedding as weights down at FWD and weight gradients up
+        at BWD (`engine.py:214-219`) because its fp16 weights live in host
+        memory (`chunks.py:204-224`, `scenario.py:133`); here a GPU-computed
+        embedding keeps weights, gradients and optimizer state resident in
+        HBM (charged to the GPU pool, ``gpu_resident_bytes``), so those rows
+        have no copy behind them.  A CPU-computed embedding ships exactly the
+        activation rows it is billed (realized)."""
+        r = report if report is not None else (self.reports[-1] if self.reports else None)
+        if r is None:
+            return {}
+        emb = sum(t.bytes for t in r.transfers if t.chunk_id == "embedding")
+        realized = self.embedding_placement == CPU == self.sim.engine.embedding_device
+        return {} if realized or emb == 0 else {"embedding": emb}
 
     def step_state(self):
         return self.executor.state.read()

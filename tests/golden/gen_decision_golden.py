@@ -59,6 +59,29 @@ CASES = [
      dict(gpu_count=1, gpu_bytes=180 * 10**9), dict(capacity_elems=64 * MI), 1, [0], 3),
     ("gpt1b_cap256Mi", dict(layers=20, hidden_dim=2048, heads=16, seq_len=1024, batch=16),
      dict(gpu_count=1, gpu_bytes=180 * 10**9), dict(capacity_elems=256 * MI), 1, [0], 3),
+    # C2 at the configuration bench.py measures: per-GPU batch 32, where the
+    # plan computes the embedding on the GPU (`profiler.py:70-74`), chunk-size
+    # sweep; 160 GB is the accounting budget the GPU test runs the real step at
+    ("gpt1b_b32_cap32Mi", dict(layers=20, hidden_dim=2048, heads=16, seq_len=1024, batch=32),
+     dict(gpu_count=1, gpu_bytes=160 * 10**9), dict(capacity_elems=32 * MI), 1, [0], 3),
+    ("gpt1b_b32_cap64Mi", dict(layers=20, hidden_dim=2048, heads=16, seq_len=1024, batch=32),
+     dict(gpu_count=1, gpu_bytes=160 * 10**9), dict(capacity_elems=64 * MI), 1, [0], 3),
+    ("gpt1b_b32_cap128Mi", dict(layers=20, hidden_dim=2048, heads=16, seq_len=1024, batch=32),
+     dict(gpu_count=1, gpu_bytes=160 * 10**9), dict(capacity_elems=128 * MI), 1, [0], 3),
+    ("gpt1b_b32_cap256Mi", dict(layers=20, hidden_dim=2048, heads=16, seq_len=1024, batch=32),
+     dict(gpu_count=1, gpu_bytes=160 * 10**9), dict(capacity_elems=256 * MI), 1, [0], 3),
+    # the C3 model on one GPU (scripts/configs_sweep.py "4b_gpu")
+    ("gpt4b_p1", dict(layers=64, hidden_dim=2304, heads=16, seq_len=1024, batch=8),
+     dict(gpu_count=1, gpu_bytes=160 * 10**9), dict(capacity_elems=64 * MI), 1, [0], 3),
+    # the C4 model on one GPU (configs_sweep "12b_mixed" / "12b_ckpt"): without
+    # checkpointing the plan splits the optimizer triplets between HBM and host
+    # DRAM and the fp16 chunks are evicted and refetched every iteration
+    ("gpt12b_p1_mixed", dict(layers=60, hidden_dim=4096, heads=32, seq_len=1024, batch=8),
+     dict(gpu_count=1, gpu_bytes=160 * 10**9, cpu_bytes=1500 * 10**9),
+     dict(capacity_elems=64 * MI), 1, [0], 3),
+    ("gpt12b_p1_ckpt", dict(layers=60, hidden_dim=4096, heads=32, seq_len=1024, batch=8),
+     dict(gpu_count=1, gpu_bytes=160 * 10**9, cpu_bytes=1500 * 10**9),
+     dict(capacity_elems=64 * MI, checkpointing=True), 1, [0], 3),
     # C3 4B ZeRO at p=8 (ranks 0 and 7)
     ("gpt4b_p8", dict(layers=64, hidden_dim=2304, heads=16, seq_len=1024, batch=8),
      dict(gpu_count=8, gpu_bytes=180 * 10**9), dict(capacity_elems=64 * MI), 8, [0, 7], 3),

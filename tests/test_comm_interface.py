@@ -8,7 +8,8 @@ from paper_2108_05818_b200.native_comm import NativeChunkComm
 from paper_2108_05818_b200.payload import ChunkComm
 from paper_2108_05818_b200.trainer import ChunkTrainer
 
-METHODS = ("all_gather_slab", "reduce_scatter_avg", "all_reduce_sum", "all_reduce_avg")
+METHODS = ("all_gather_slab", "reduce_scatter_avg", "all_reduce_sum", "all_reduce_avg",
+           "check")
 
 
 def test_native_comm_mirrors_chunk_comm():

@@ -34,8 +34,7 @@ def _oracle_state(O, st: "K.N.CsStepState"):
     return s
 
 
-@pytest.fixture(params=[0, 2, 5, 6, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23,
-                        24],
+@pytest.fixture(params=[0, 1],
                 ids=lambda v: "variant%d" % v)
 def adam_variant(request, native_lib):
     old = native_lib.cs_adam_variant(-1)
@@ -76,7 +75,10 @@ def test_adam_chunks_bit_exact(native_lib, oracle_lib, adam_variant, dtype, wd, 
 
 
 def test_adam_chunks_many_items_and_prefix_only(native_lib, oracle_lib, adam_variant):
-    """300 items (two launches); only the used prefix of each chunk changes."""
+    """300 items plus 43 zero-length ones interleaved (two launches, the
+    batch boundary falls among empty items); only the used prefix of each
+    chunk changes and every item is updated exactly once (a double update
+    would not match the oracle's single step)."""
     O = oracle_lib
     cap, used = 8192, 5000
     hyper = K.AdamHyper(lr=1e-3)
@@ -93,7 +95,13 @@ def test_adam_chunks_many_items_and_prefix_only(native_lib, oracle_lib, adam_var
         v = torch.zeros(cap)
         chunks.append([x.to(DEV) for x in (p16, p32, m, v)] + [x.numpy().copy() for x in (p32, m, v)]
                       + [_bits16(p16)])
-    K.adam_chunks([(c[0], c[1], c[2], c[3], used) for c in chunks], hyper, state)
+    items = []
+    for i, c in enumerate(chunks):
+        items.append((c[0], c[1], c[2], c[3], used))
+        if i % 7 == 3:  # an empty item takes no batch slot
+            items.append((c[0], c[1], c[2], c[3], 0))
+    assert len(items) > 256 + 30
+    K.adam_chunks(items, hyper, state)
     torch.cuda.synchronize()
     for c in chunks:
         rp, rm, rv, rg = c[4], c[5], c[6], c[7]
@@ -479,3 +487,54 @@ def test_k1_at_the_bench_layout_every_element_bit_exact(native_lib, oracle_lib):
             assert np.array_equal(v[a:b].cpu().numpy().view(np.uint32), rv.view(np.uint32))
         # the unused tail of each chunk is never touched
         assert torch.equal(p16[n:], t16) and torch.equal(p32[n:], t32)
+
+
+def test_sumsq_and_pack_with_zero_length_items_across_batches(native_lib):
+    """K2 and K3/K4 work lists longer than one launch's batch with empty
+    items mixed in: every non-empty item is counted / packed exactly once."""
+    gen = torch.Generator().manual_seed(11)
+    grads, items = [], []
+    for i in range(300):
+        g = (torch.randn(1000 + i, generator=gen) * 0.1).half().to(DEV)
+        grads.append(g)
+        items.append((g, g.numel()))
+        if i % 5 == 0:
+            items.append((g, 0))
+    assert len(items) > 256 + 30
+    partials = torch.zeros(K.sumsq_partials() + 1, device=DEV)
+    K.grad_sumsq(items, partials[:-1], dtype=torch.float16)
+    want = sum(float((g.double() ** 2).sum()) for g in grads)
+    assert abs(float(partials[:-1].double().sum()) - want) <= 1e-4 * want  # fp32 partials
+    for acc in (0, 1):
+        dst = torch.zeros(sum(g.numel() for g in grads), dtype=torch.float16, device=DEV)
+        pk, off = [], 0
+        for g in grads:
+            pk.append((dst, off, g, g.numel()))
+            pk.append((dst, off, g, 0))
+            off += g.numel()
+        K.pack(pk, accumulate=bool(acc))
+        torch.cuda.synchronize()
+        assert torch.equal(dst, torch.cat(grads)), acc
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_nan_masters_narrow_like_the_host(native_lib, adam_variant, dtype):
+    """A NaN master narrows to the same 16-bit pattern on the device (K1)
+    and on the host (cs_adam_chunks_host): the canonical NaN 0x7fff."""
+    n = 4096 + 24
+    bits = np.array([0x7fc00000, 0xffc00000, 0x7fffffff, 0xffffffff, 0x7f800001, 0x7fbfffff,
+                     0xff800001, 0x7ff0f0f0], dtype=np.uint32)
+    p = np.resize(bits, n).view(np.float32)
+    hyper = K.AdamHyper()
+    state = K.StepState(DEV)
+    state.sumsq().fill_(1.0)
+    K.adam_prepare(state, hyper)
+    dev = [torch.zeros(n, dtype=dtype, device=DEV), torch.from_numpy(p.copy()).to(DEV),
+           torch.zeros(n, device=DEV), torch.zeros(n, device=DEV)]
+    K.adam_chunks([(*dev, n)], hyper, state)
+    host = [torch.zeros(n, dtype=dtype), torch.from_numpy(p.copy()), torch.zeros(n),
+            torch.zeros(n)]
+    K.adam_chunks_host([(*host, n)], hyper, state.read(), n_threads=2)
+    torch.cuda.synchronize()
+    assert np.array_equal(_bits16(dev[0]), _bits16(host[0]))
+    assert (_bits16(dev[0]) == 0x7fff).all(), hex(int(_bits16(dev[0])[0]))

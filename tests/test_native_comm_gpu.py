@@ -54,7 +54,19 @@ def _worker(rank, port, out):
             res["noncontig"] = "rejected"
         rc = lib.cs_allgather(None, None, 4, N.CS_FP16, comm._comm, None)
         res["einval"] = rc
+        w = comm.reduce_scatter_avg(mine, slab, async_op=True)
+        w.wait_host(timeout_s=60)                         # polls the async error
+        res["check"] = lib.cs_comm_check(comm._comm)
         torch.cuda.synchronize()
+        from paper_2108_05818_b200.native_comm import NcclAsyncError
+        comm2 = NativeChunkComm(None, torch.device("cuda:0"))
+        comm2.abort()                                      # ncclCommAbort
+        try:
+            comm2.all_gather_slab(torch.zeros(16, device="cuda").half())
+            res["after_abort"] = "accepted"
+        except NcclAsyncError:
+            res["after_abort"] = "raised"
+        res["check_null"] = lib.cs_comm_check(None)
         comm.close()
     finally:
         dist.destroy_process_group()
@@ -75,3 +87,5 @@ def test_native_communicator_single_rank_round_trip():
     assert res["calls"] == ["all_gather", "reduce_scatter"] * 2
     assert res["noncontig"] == "rejected"
     assert res["einval"] == -1
+    assert res["check"] == 0 and res["check_null"] == -1
+    assert res["after_abort"] == "raised"
