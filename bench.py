@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-offload-probe", action="store_true",
                     help="skip the host-offload side measurement (chunk moves GB/s)")
     ap.add_argument("--cpu-sample-batch", type=int, default=1)
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the C5 microbench summary (K1-K6 1M-1G elements + CPU Adam arms)")
     ap.add_argument("--profile-step", action="store_true",
                     help="after warm-up run ONE step between cudaProfilerStart/Stop and exit "
                          "(for ncu --profile-from-start off); prints no bench line")
@@ -215,6 +217,55 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
     return out
 
 
+def c5_probe(sizes=(20, 22, 24, 26, 28, 30), oracle_sizes=(20, 24)):
+    """C5 (BASELINE.json configs[4]): K1 fused chunk Adam at 1M-1G elements,
+    L2 flushed before every launch, HBM GB/s vs the measured peak; beside it
+    the CPU Adam arms on the same element counts (torch-CPU fused Adam with
+    the chunk casts, all threads; this build's host K1; the C oracle, one
+    thread per core, at the small sizes only)."""
+    import torch
+    from paper_2108_05818_b200 import microbench as MB
+    rows = MB.run(list(sizes), iters=5, kernels=("adam", "sumsq", "pack", "accumulate",
+                                                  "cast_pack", "master_init"))
+    torch.cuda.empty_cache()
+    table = {}
+    for r in rows:
+        e = table.setdefault(str(r["n"]), {})
+        e[r["kernel"]] = {"gpu_gbs": r["gbs"], "gpu_frac": r["frac_of_measured_peak"],
+                          "regime": r["regime"]}
+    for lg in sizes:
+        n = 1 << lg
+        it = 1 if n >= (1 << 29) else 2
+        a = MB.cpu_torch_fused_adam(n, it)
+        b = MB.cpu_host_k1(n, it)
+        table[str(n)]["adam"].update({"cpu_torch_fused_gbs": a["gbs"],
+                                      "cpu_torch_fused_threads": a["threads"],
+                                      "cpu_host_k1_gbs": b["gbs"],
+                                      "cpu_host_k1_threads": b["threads"]})
+    for lg in oracle_sizes:  # the C restatement (checker), scalar
+        import numpy as np
+        import time as _t
+        from oracle import numerics as O
+        n = 1 << lg
+        rng = np.random.default_rng(0)
+        g = O.to_half_bits((rng.standard_normal(n) * 1e-3).astype(np.float32))
+        p32 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+        m, v = np.zeros(n, np.float32), np.zeros(n, np.float32)
+        st = O.step_state(1.0)
+        O.adam_prepare(st, 1e-4, 0.9, 0.999)
+        thr = len(os.sched_getaffinity(0))
+        t0 = _t.perf_counter()
+        O.adam(g, p32, m, v, n, O.FP16, 1e-4, 0.9, 0.999, 1e-8, 0.0, False, st, threads=thr)
+        dt = _t.perf_counter() - t0
+        table[str(n)]["adam"].update({"cpu_oracle_gbs": round(28 * n / dt / 1e9, 3),
+                                      "cpu_oracle_threads": thr})
+    return {"kernels_bytes_per_elem": MB.BYTES_PER_ELEM, "peak_gbs": MB.measured_peak_gbs(),
+            "l2": "flushed (2 x 126 MB write) before every GPU launch",
+            "cpu_arms": "torch.optim.Adam(fused=True) on CPU incl. fp16->fp32 grad and "
+                        "fp32->fp16 param casts; cs_adam_chunks_host (AVX2+OpenMP); C oracle "
+                        "(scalar C, OpenMP over the affinity mask)", "rows": table}
+
+
 NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md; 900 nominal)
 
 
@@ -259,6 +310,40 @@ def collective_probe(dev, cap, dtype, world, iters=5, warmup=2):
     return res
 
 
+def collectives_in_step(durations, world, steps):
+    """Per kind: count per step, mean ms and busbw of the chunk-group
+    collectives as they ran inside the timed steps (overlapped with compute),
+    busbw = (p-1) * slot bytes / duration, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    kinds = ("all_gather", "reduce_scatter_avg")
+    agg = {k: [0, 0.0, 0] for k in kinds}  # count, ms, wire bytes
+    src = "none"
+    for kind, nbytes, ms, how in durations:
+        a = agg.setdefault(kind, [0, 0.0, 0])
+        a[0] += 1
+        a[1] += ms
+        a[2] += (world - 1) * nbytes // world
+        src = how
+    t = torch.tensor([agg[k][1] for k in kinds], dtype=torch.float64,
+                     device=torch.cuda.current_device())
+    if dist.get_backend() == "gloo":
+        t = t.cpu()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    res = {}
+    for i, k in enumerate(kinds):
+        n, _, wire = agg[k]
+        ms = float(t[i])
+        busbw = wire / (ms * 1e-3) / 1e9 if ms > 0 else None
+        res[k] = {"per_step": n / max(steps, 1), "mean_ms": round(ms / n, 4) if n else None,
+                  "busbw_gbs": round(busbw, 1) if busbw else None,
+                  "frac": round(busbw / NVLINK_PEAK_GBS, 4) if busbw else None}
+    res["timing"] = ("Work.get_duration (NCCL-stream events)" if src == "work" else
+                     "CUDA events from issue to completion (includes queueing behind earlier "
+                     "collectives)")
+    return res
+
+
 def k1_traffic(elements):
     """Per-launch DRAM traffic of K1 from the committed `ncu --set full`
     capture of the same in-step launch (profiles/), scaled to this launch's
@@ -288,6 +373,72 @@ def cpu_baseline(schema_kw, sample_batch, steps=1):
                                                schema.hidden_dim,
                                                sum(p.numel() for p in runner.model.parameters())
                                                / 1e9, steps)}
+
+
+REF_ENGINE_CODE = r"""
+import json, sys, time
+sys.path.insert(0, sys.argv[1])
+import chunkstar
+from chunkstar.config import HardwareSpec, PolicySpec
+from chunkstar.model import build_gpt_schema
+from chunkstar.scenario import Simulator
+assert chunkstar.__file__.startswith(sys.argv[1]), chunkstar.__file__
+kw = json.loads(sys.argv[2])
+schema = build_gpt_schema(**kw["schema"])
+sim = Simulator(schema, HardwareSpec(gpu_count=1, gpu_bytes=kw["gpu_bytes"]),
+                PolicySpec(capacity_elems=kw["cap"]), 1)
+t0 = time.perf_counter()
+warm = sim.engine.run_iteration(0, warmup=True, plan_builder=sim._plan_builder())
+t1 = time.perf_counter()
+secs = []
+for i in range(1, 1 + kw["iters"]):
+    a = time.perf_counter()
+    r = sim.engine.run_iteration(i, warmup=False)
+    secs.append(time.perf_counter() - a)
+    assert r.feasible
+print(json.dumps({"warmup_s": t1 - t0, "measured_s": secs, "events": len(sim.timeline.events),
+                  "pcie_bytes": r.pcie_bytes}))
+"""
+
+
+def decision_engine_timing(args, iters=3):
+    """SURVEY §8(d) CPU baseline item 1: the UNMODIFIED reference's
+    `Engine.run_iteration` (`cs/engine.py:282-364`, installed under
+    baseline/_ref) on the bench's timeline, one Python thread, beside this
+    build's decision engine (accounting-only) on the same timeline."""
+    import subprocess
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    schema = dict(layers=args.layers, hidden_dim=args.hidden, heads=args.heads,
+                  seq_len=args.seq, vocab=args.vocab, batch=args.batch)
+    kw = {"schema": schema, "cap": args.cap, "gpu_bytes": 160 * 10**9, "iters": iters}
+    out = {"config": "GPT L%d H%d B%d cap %d, 160 GB accounting budget"
+                     % (args.layers, args.hidden, args.batch, args.cap)}
+    if os.path.isdir(os.path.join(ref_dir, "chunkstar")):
+        res = subprocess.run([sys.executable, "-c", REF_ENGINE_CODE, ref_dir, json.dumps(kw)],
+                             capture_output=True, text=True, timeout=900)
+        if res.returncode == 0:
+            d = json.loads(res.stdout.strip().splitlines()[-1])
+            out["reference_ms_per_iteration"] = round(1e3 * min(d["measured_s"]), 2)
+            out["reference_warmup_ms"] = round(1e3 * d["warmup_s"], 2)
+            out["events"] = d["events"]
+        else:
+            out["reference_error"] = res.stderr[-300:]
+    else:
+        out["reference_error"] = "baseline/_ref not installed"
+    from paper_2108_05818_b200.config import HardwareSpec, PolicySpec
+    from paper_2108_05818_b200.model import build_gpt_schema
+    from paper_2108_05818_b200.scenario import Simulator
+    sim = Simulator(build_gpt_schema(**schema), HardwareSpec(gpu_count=1, gpu_bytes=kw["gpu_bytes"]),
+                    PolicySpec(capacity_elems=args.cap), 1)
+    sim.engine.run_iteration(0, warmup=True, plan_builder=sim._plan_builder())
+    secs = []
+    for i in range(1, 1 + iters):
+        a = time.perf_counter()
+        sim.engine.run_iteration(i, warmup=False)
+        secs.append(time.perf_counter() - a)
+    out["this_build_ms_per_iteration"] = round(1e3 * min(secs), 2)
+    out["threads"] = 1
+    return out
 
 
 def run_reference(args):
@@ -320,6 +471,10 @@ def run_reference(args):
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    try:
+        line["decision_engine"] = decision_engine_timing(args)
+    except Exception as e:  # reported, never fatal
+        line["decision_engine"] = {"error": repr(e)[:300]}
     print(json.dumps(line), flush=True)
 
 
@@ -345,6 +500,9 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         if args.dist_backend == "nccl":
+            # per-collective start/end events on the NCCL stream: the in-step
+            # durations of the chunk-group collectives (Work.get_duration)
+            os.environ.setdefault("TORCH_NCCL_ENABLE_TIMING", "1")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(args.dist_backend)
@@ -384,6 +542,9 @@ def main():
     # ---- timed region 1: device-resident inputs -> value -----------------------
     ex.record_k1 = True
     ex.k1_events.clear()
+    if world > 1:  # in-step durations of the overlapped chunk-group collectives
+        ex.time_collectives = True
+        ex.coll_log.clear()
     moved0 = ex.stats.h2d_bytes - ex.stats.prefetch_discarded_bytes + ex.stats.d2h_bytes
     reports0 = len(trainer.reports)
     launches0 = _native.launch_count()
@@ -406,6 +567,11 @@ def main():
     if trainer._graph is not None:  # library kernels replayed from the captured graph
         launches += trainer.graph_kernels_per_step * args.steps
     ms = t0.elapsed_time(t1) / args.steps
+    in_step = None
+    if world > 1:
+        ex.time_collectives = False
+        in_step = collectives_in_step(ex.collective_durations(), world, args.steps)
+        ex.coll_log.clear()
     # chunk bytes the executor moved in the timed steps (a replayed graph
     # moves none: it is only captured once the schedule moves no chunk)
     moved = (ex.stats.h2d_bytes - ex.stats.prefetch_discarded_bytes + ex.stats.d2h_bytes
@@ -530,6 +696,7 @@ def main():
             out["collectives"] = collective_probe(dev, args.cap, dtype, world)
         except Exception as e:  # reported, never fatal
             out["collectives"] = {"error": repr(e)[:300]}
+        out["collectives"]["in_step"] = in_step
     if world == 1 and not args.no_offload_probe:
         del trainer, ex
         torch.cuda.empty_cache()
@@ -537,6 +704,12 @@ def main():
             out["offload_probe"] = offload_probe(schema_kw, dev)
         except Exception as e:  # reported, never fatal
             out["offload_probe"] = {"error": repr(e)[:300]}
+    if world == 1 and not args.no_c5:
+        torch.cuda.empty_cache()
+        try:
+            out["c5"] = c5_probe()
+        except Exception as e:  # reported, never fatal
+            out["c5"] = {"error": repr(e)[:300]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             out["cpu_baseline"] = cpu_baseline(schema_kw, args.cpu_sample_batch)

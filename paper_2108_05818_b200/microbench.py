@@ -1,19 +1,35 @@
-"""C5 microbench: chunk kernels K1-K6 at 1M-1G elements, HBM GB/s vs roofline.
+"""C5 microbench (BASELINE.json configs[4]): chunk kernels K1-K6 at
+1M-1G elements, HBM GB/s vs roofline, beside CPU Adam arms.
 
 Algorithmic bytes per element: K1 Adam 28, K2 sumsq 2,
 K3 pack 4, K4 accumulate 6, K5 cast+pack 6, K6 state birth 14 (fp16 src).
-Each kernel is timed with CUDA events around a CUDA-graph replay of
-``iters`` back-to-back launches after warm-up (device time, no host launch
-cost); inputs >= 8M elements exceed the 126 MB L2 between iterations,
-smaller ones partly hit L2.
 
-    python -m paper_2108_05818_b200.microbench [--sizes 20,22,...] [--iters N]
+GPU arm: every timed launch is preceded by an L2 flush (a write of a
+buffer twice the 126 MB L2), and bracketed by CUDA events on its stream;
+the flush's ~0.1 ms of device work hides the host launch, so the events
+see the kernel alone, cold.  Sizes below ~4M elements are latency-bound
+(a few microseconds of launch ramp against < 10 us of traffic) and are
+labelled so; the roofline fraction is meaningful from 16M elements up.
+
+CPU arms (SURVEY §8d CPU baseline items 2-3), same element counts, same
+28 B/element of algorithmic traffic, host DRAM:
+
+* ``cpu_torch_fused``: torch-CPU fused Adam (``torch.optim.Adam(fused=True)``
+  over the fp32 master) with the chunk path's casts — fp16 gradients widened
+  to fp32 before, the fp16 parameter copy narrowed after;
+* ``cpu_host_k1``: this build's own host K1 (``cs_adam_chunks_host``, AVX2 +
+  OpenMP), the kernel that runs CPU-placed optimizer triplets.
+
+Thread counts are reported with every CPU row.
+
+    python -m paper_2108_05818_b200.microbench [--sizes 20,22,...] [--iters N] [--cpu]
 """
 
 import argparse
 import json
 import os
-from typing import Callable, Dict, List
+import time
+from typing import Callable, Dict, List, Optional
 
 import torch
 
@@ -21,6 +37,8 @@ from . import kernels as K
 
 BYTES_PER_ELEM = {"adam": 28, "sumsq": 2, "pack": 4, "accumulate": 6, "cast_pack": 6,
                   "master_init": 14}
+L2_BYTES = 126 << 20
+LATENCY_BOUND_BELOW = 1 << 24  # elements
 
 
 def measured_peak_gbs() -> float:
@@ -33,30 +51,37 @@ def measured_peak_gbs() -> float:
         return 6650.0  # B200_PROFILING.md fallback
 
 
-def time_launch(fn: Callable[[], None], iters: int, warmup: int = 3) -> float:
-    """Average DEVICE milliseconds per call: the ``iters`` calls are captured
-    once into a CUDA graph and replayed between CUDA events, so small sizes
-    measure the kernel, not the Python/ctypes launch path."""
+class L2Flush:
+    """Writes a buffer of 2 x L2 so the next launch starts cold."""
+
+    def __init__(self, device="cuda"):
+        self.buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=device)
+
+    def __call__(self) -> None:
+        self.buf.fill_(1.0)
+
+
+def time_launch(fn: Callable[[], None], iters: int, flush: Optional[L2Flush],
+                warmup: int = 2) -> float:
+    """Average DEVICE milliseconds per cold call (see the module doc)."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=side):
-        for _ in range(iters):
-            fn()
-    graph.replay()  # warm replay
+    pairs = []
+    for _ in range(iters):
+        if flush is not None:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        pairs.append((a, b))
     torch.cuda.synchronize()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
-    graph.replay()
-    end.record()
-    torch.cuda.synchronize()
-    return start.elapsed_time(end) / iters
+    return sum(a.elapsed_time(b) for a, b in pairs) / iters
 
 
-def bench_size(n: int, iters: int, dtype=torch.float16) -> Dict[str, float]:
+def bench_size(n: int, iters: int, dtype=torch.float16, flush: Optional[L2Flush] = None,
+               kernels=tuple(BYTES_PER_ELEM)) -> Dict[str, float]:
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(0)
     p16 = (torch.randn(n, device=dev, generator=g) * 1e-3).to(dtype)
@@ -68,55 +93,111 @@ def bench_size(n: int, iters: int, dtype=torch.float16) -> Dict[str, float]:
     state.sumsq().fill_(1.0)
     K.adam_prepare(state, hyper)
     partials = torch.empty(K.sumsq_partials(), device=dev)
-    src16 = (torch.randn(n, device=dev, generator=g)).to(dtype)
-    src32 = torch.randn(n, device=dev, generator=g)
-    out = {}
-    ms = time_launch(lambda: K.adam_chunks([(p16, p32, m, v, n)], hyper, state), iters)
-    out["adam"] = ms
-    out["sumsq"] = time_launch(lambda: K.grad_sumsq([(p16, n)], partials), iters)
-    out["pack"] = time_launch(lambda: K.pack([(p16, 0, src16, n)]), iters)
-    out["accumulate"] = time_launch(lambda: K.pack([(p16, 0, src16, n)], accumulate=True), iters)
-    out["cast_pack"] = time_launch(lambda: K.cast_pack([(p16, 0, src32, n)]), iters)
-    out["master_init"] = time_launch(lambda: K.master_init(p32, m, v, p16, n), iters)
-    return out
+    fns = {"adam": lambda: K.adam_chunks([(p16, p32, m, v, n)], hyper, state),
+           "sumsq": lambda: K.grad_sumsq([(p16, n)], partials)}
+    if any(k in kernels for k in ("pack", "accumulate", "cast_pack", "master_init")):
+        src16 = (torch.randn(n, device=dev, generator=g)).to(dtype)
+        src32 = torch.randn(n, device=dev, generator=g)
+        fns.update({"pack": lambda: K.pack([(p16, 0, src16, n)]),
+                    "accumulate": lambda: K.pack([(p16, 0, src16, n)], accumulate=True),
+                    "cast_pack": lambda: K.cast_pack([(p16, 0, src32, n)]),
+                    "master_init": lambda: K.master_init(p32, m, v, p16, n)})
+    return {k: time_launch(fns[k], iters, flush) for k in kernels}
 
 
-def run(sizes_log2: List[int], iters: int) -> List[dict]:
+def run(sizes_log2: List[int], iters: int, kernels=tuple(BYTES_PER_ELEM)) -> List[dict]:
     peak = measured_peak_gbs()
+    flush = L2Flush()
     rows = []
     for lg in sizes_log2:
         n = 1 << lg
-        times = bench_size(n, iters)
+        times = bench_size(n, iters, flush=flush, kernels=kernels)
         for name, ms in times.items():
             gbs = BYTES_PER_ELEM[name] * n / (ms * 1e-3) / 1e9
-            rows.append({"kernel": name, "n": n, "ms": round(ms, 5), "gbs": round(gbs, 1),
-                         "frac_of_measured_peak": round(gbs / peak, 4)})
+            rows.append({"arm": "gpu", "kernel": name, "n": n, "ms": round(ms, 5),
+                         "gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4),
+                         "regime": "latency-bound" if n < LATENCY_BOUND_BELOW else "hbm",
+                         "l2": "flushed before every launch"})
         torch.cuda.empty_cache()
+    return rows
+
+
+# ---- CPU arms ------------------------------------------------------------------------
+
+
+def _cpu_inputs(n: int):
+    g = torch.Generator().manual_seed(0)
+    g16 = (torch.randn(n, generator=g) * 1e-3).half()
+    p32 = torch.randn(n, generator=g) * 0.02
+    m = torch.randn(n, generator=g) * 1e-4
+    v = torch.rand(n, generator=g) * 1e-7
+    return g16, p32, m, v
+
+
+def cpu_torch_fused_adam(n: int, iters: int = 2) -> dict:
+    """torch-CPU fused Adam with the chunk path's casts, all host threads."""
+    g16, p32, m, v = _cpu_inputs(n)
+    p = torch.nn.Parameter(p32)
+    opt = torch.optim.Adam([p], lr=1e-4, betas=(0.9, 0.999), eps=1e-8, fused=True)
+    p16 = torch.empty(n, dtype=torch.float16)
+    times = []
+    for k in range(iters + 1):
+        t0 = time.perf_counter()
+        p.grad = g16.float()          # fp16 grad chunk widened on the fly
+        opt.step()
+        p16.copy_(p.detach())         # fp32 master narrowed into the fp16 chunk
+        if k:
+            times.append(time.perf_counter() - t0)
+    s = min(times)
+    return {"arm": "cpu_torch_fused", "kernel": "adam", "n": n, "ms": round(s * 1e3, 3),
+            "gbs": round(28 * n / s / 1e9, 2), "gelem_per_s": round(n / s / 1e9, 4),
+            "threads": torch.get_num_threads()}
+
+
+def cpu_host_k1(n: int, iters: int = 2, threads: int = 0) -> dict:
+    """This build's host K1 (AVX2/F16C + OpenMP) over pinned host buffers."""
+    from . import _native as N
+    g16, p32, m, v = _cpu_inputs(n)
+    if torch.cuda.is_available():  # the buffers CPU-placed triplets live in
+        g16, p32, m, v = (t.pin_memory() for t in (g16, p32, m, v))
+    st = N.CsStepState()
+    st.grad_scale, st.step_size, st.sqrt_bc2, st.skip = 1.0, 1e-4, 0.03, 0
+    hyper = K.AdamHyper(lr=1e-4)
+    times = []
+    for k in range(iters + 1):
+        t0 = time.perf_counter()
+        K.adam_chunks_host([(g16, p32, m, v, n)], hyper, st, threads)
+        if k:
+            times.append(time.perf_counter() - t0)
+    s = min(times)
+    return {"arm": "cpu_host_k1", "kernel": "adam", "n": n, "ms": round(s * 1e3, 3),
+            "gbs": round(28 * n / s / 1e9, 2), "gelem_per_s": round(n / s / 1e9, 4),
+            "threads": int(N.load().cs_host_threads(threads))}
+
+
+def run_cpu(sizes_log2: List[int]) -> List[dict]:
+    rows = []
+    for lg in sizes_log2:
+        n = 1 << lg
+        it = 1 if n >= (1 << 29) else 2
+        rows.append(cpu_torch_fused_adam(n, it))
+        rows.append(cpu_host_k1(n, it))
     return rows
 
 
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="20,22,24,26,28,30")
-    ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--adam-variants", default="",
-                    help="comma list of cs_adam_variant ids: time K1 for each")
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--cpu", action="store_true", help="also run the CPU Adam arms")
+    ap.add_argument("--kernels", default=",".join(BYTES_PER_ELEM))
     args = ap.parse_args()
-    if args.adam_variants:
-        from . import _native as N
-        peak = measured_peak_gbs()
-        for v in [int(x) for x in args.adam_variants.split(",")]:
-            N.load().cs_adam_variant(v)
-            for lg in [int(s) for s in args.sizes.split(",")]:
-                n = 1 << lg
-                ms = bench_size(n, args.iters)["adam"]
-                gbs = 28 * n / (ms * 1e-3) / 1e9
-                print(json.dumps({"kernel": "adam", "variant": v, "n": n, "ms": round(ms, 5),
-                                  "gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4)}))
-        return
-    rows = run([int(s) for s in args.sizes.split(",")], args.iters)
-    for r in rows:
-        print(json.dumps(r))
+    sizes = [int(s) for s in args.sizes.split(",")]
+    for r in run(sizes, args.iters, tuple(args.kernels.split(","))):
+        print(json.dumps(r), flush=True)
+    if args.cpu:
+        for r in run_cpu(sizes):
+            print(json.dumps(r), flush=True)
 
 
 if __name__ == "__main__":

@@ -31,11 +31,17 @@ class NcclAsyncError(RuntimeError):
 
 
 class _Work:
-    __slots__ = ("_event", "_comm")
+    __slots__ = ("_event", "_comm", "_start")
 
-    def __init__(self, event: torch.cuda.Event, comm: "NativeChunkComm"):
+    def __init__(self, event: torch.cuda.Event, comm: "NativeChunkComm",
+                 start: Optional[torch.cuda.Event] = None):
         self._event = event
         self._comm = comm
+        self._start = start
+
+    def get_duration(self) -> float:
+        """Milliseconds the collective ran on the comm stream (after it)."""
+        return self._start.elapsed_time(self._event)
 
     def wait(self) -> None:
         torch.cuda.current_stream().wait_event(self._event)
@@ -127,10 +133,12 @@ class NativeChunkComm:
         self.stream.wait_stream(cur)
         for t in tensors:  # the caching allocator must not recycle them under the op
             t.record_stream(self.stream)
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(self.stream)
         call(ctypes.c_void_p(self.stream.cuda_stream))
-        ev = torch.cuda.Event()
+        ev = torch.cuda.Event(enable_timing=True)
         ev.record(self.stream)
-        work = _Work(ev, self)
+        work = _Work(ev, self, start)
         if async_op:
             return work
         work.wait()
@@ -142,16 +150,24 @@ class NativeChunkComm:
             raise ValueError("native collectives take contiguous CUDA fp16/bf16/fp32 tensors")
         return CODE[t.dtype]
 
-    def all_gather_slab(self, slab: torch.Tensor, async_op: bool = False):
-        """In place: slot ``rank`` of ``slab`` is this rank's contribution."""
+    def all_gather_slab(self, slab: torch.Tensor, async_op: bool = False,
+                        src: Optional[torch.Tensor] = None):
+        """This rank's contribution is ``src`` (out of place) or slot ``rank``
+        of ``slab`` (in place)."""
         cap = slab.numel() // self.world
         code = self._code(slab)
-        mine = slab.data_ptr() + self.rank * cap * slab.element_size()
+        keep = (slab,)
+        if src is None:
+            mine = slab.data_ptr() + self.rank * cap * slab.element_size()
+        else:
+            if self._code(src) != code or src.numel() < cap:
+                raise ValueError("all_gather_slab: src must hold one slot of the slab's dtype")
+            mine, keep = src.data_ptr(), (slab, src)
         self.calls.append(("all_gather", slab.numel() * slab.element_size()))
         lib = N.load()
         return self._run(lambda s: N.check(lib.cs_allgather(slab.data_ptr(), mine, cap, code,
                                                             self._comm, s), "cs_allgather"),
-                         async_op, slab)
+                         async_op, *keep)
 
     def reduce_scatter_avg(self, out: torch.Tensor, slab: torch.Tensor, async_op: bool = False):
         code = self._code(slab)

@@ -70,12 +70,15 @@ class ChunkComm:
         self.rank = dist.get_rank(group)
         self.calls: List[Tuple[str, int]] = []
 
-    def all_gather_slab(self, slab: torch.Tensor, async_op: bool = False):
-        """In place: slot ``rank`` of ``slab`` is this rank's contribution.
-        With ``async_op`` returns the Work; ``work.wait()`` orders the
-        caller's current stream after it (no host wait on NCCL)."""
+    def all_gather_slab(self, slab: torch.Tensor, async_op: bool = False,
+                        src: Optional[torch.Tensor] = None):
+        """Gather every rank's chunk into ``slab``.  This rank's contribution
+        is ``src`` (out of place: NCCL places it in slot ``rank`` itself, no
+        staging copy), or slot ``rank`` of ``slab`` when ``src`` is None (in
+        place).  With ``async_op`` returns the Work; ``work.wait()`` orders
+        the caller's current stream after it (no host wait on NCCL)."""
         cap = slab.numel() // self.world
-        mine = slab[self.rank * cap:(self.rank + 1) * cap]
+        mine = slab[self.rank * cap:(self.rank + 1) * cap] if src is None else src[:cap]
         self.calls.append(("all_gather", slab.numel() * slab.element_size()))
         return dist.all_gather_into_tensor(slab, mine, group=self.group, async_op=async_op)
 
@@ -200,6 +203,12 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._last_bwd_at: Optional[Dict[int, List[int]]] = None  # event -> positions
         self._drain_candidates: List[int] = []
         self._rs_out: Set[int] = set()  # local chunks whose reduce-scatter was issued
+        #: in-step collective timing (bench at N > 1): every chunk-group
+        #: collective's (kind, slab bytes, Work, start event) is logged; the
+        #: duration is the Work's own (torch's NCCL with TORCH_NCCL_ENABLE_TIMING,
+        #: the native communicator's comm-stream events), else issue -> done
+        self.time_collectives = False
+        self.coll_log: List[tuple] = []
         self._stats_lock = threading.Lock()
         #: CPU-placed embedding operator (embedding.HostEmbedding) or None
         self.host_embedding = None
@@ -585,20 +594,63 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         slab = torch.empty(p * cap, dtype=self.dtype, device=self.device)
         mine = self._group_slot(slab, self.rank)
         pos = group.member_positions[self.rank]
+        src = None
         if pos is None:
             mine.zero_()  # phantom slot of a padded tail group
         else:
             local = self.chunk_set.param_chunk(pos)
-            if self.has(local, GPU):
+            if self.has(local, GPU):  # sent straight from the chunk (out of place)
                 self.wait_ready(local, GPU)
-                mine.copy_(self.tensor(local, GPU))
+                src = self.tensor(local, GPU)
             else:  # local payload lives on the host: stage it into our slot
                 self.wait_ready(local, CPU)
                 mine.copy_(self.tensor(local, CPU), non_blocking=True)
-        work = self.comm.all_gather_slab(slab, async_op=self.overlap_collectives)
+        t0 = self._coll_start()
+        work = self.comm.all_gather_slab(slab, async_op=self.overlap_collectives, src=src)
         if work is not None:
             self._inflight.append((work, (slab,)))
+        self._coll_end("all_gather", slab, work, t0)
         return slab, work
+
+    def _coll_start(self):
+        if not self.time_collectives:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def _coll_end(self, kind: str, slab: torch.Tensor, work, t0) -> None:
+        if t0 is None:
+            return
+        end = None
+        if work is None or not hasattr(work, "get_duration"):
+            end = torch.cuda.Event(enable_timing=True)
+            if work is not None:  # completion, seen from a side stream
+                if not hasattr(self, "_timing_stream"):
+                    self._timing_stream = torch.cuda.Stream(self.device)
+                with torch.cuda.stream(self._timing_stream):
+                    work.wait()
+                    end.record()
+            else:
+                end.record()
+        self.coll_log.append((kind, slab.numel() * slab.element_size(), work, t0, end))
+
+    def collective_durations(self) -> List[Tuple[str, int, float, str]]:
+        """(kind, slab bytes, ms, source) of every logged collective; call
+        after the device finished them."""
+        out = []
+        for kind, nbytes, work, t0, end in self.coll_log:
+            ms, src = None, "events"
+            if end is None:
+                try:
+                    ms, src = float(work.get_duration()), "work"
+                except Exception:
+                    ms = None
+            if ms is None and end is not None:
+                ms = t0.elapsed_time(end)
+            if ms is not None:
+                out.append((kind, nbytes, ms, src))
+        return out
 
     def all_gather(self, group: CommGroup, kind: str) -> None:
         if self.comm is None:
@@ -645,7 +697,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 slot.copy_(src)
         if out is None:
             out = torch.empty(cap, dtype=self.dtype, device=self.device)  # phantom owner
+        t0 = self._coll_start()
         work = self.comm.reduce_scatter_avg(out, slab, async_op=self.overlap_collectives)
+        self._coll_end("reduce_scatter_avg", slab, work, t0)
         if work is not None:  # overlaps the next groups' backward; waited at first use
             self._inflight.append((work, (slab, out)))
             if out_cid is not None:

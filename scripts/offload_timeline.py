@@ -1,0 +1,132 @@
+"""Timeline of the all-host-optimizer-state step (bench offload probe config).
+
+Records, for one steady-state step: the GPU start time of every timeline
+event (CUDA event on the compute stream), every chunk copy's GPU window
+(copy-stream events) and every host Adam job's host window, relative to the
+step start.  Prints a compact JSON summary; ``--ab`` alternates early
+gradient drain on/off and prints ms/step for each.
+
+    python scripts/offload_timeline.py [--batch 32] [--ab 3]
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2108_05818_b200 import kernels as K  # noqa: E402
+from paper_2108_05818_b200.config import PolicySpec  # noqa: E402
+from paper_2108_05818_b200.model import build_gpt_schema  # noqa: E402
+from paper_2108_05818_b200.trainer import ChunkTrainer  # noqa: E402
+
+
+def make(batch, env):
+    os.environ.update(env)
+    schema = build_gpt_schema(layers=20, hidden_dim=2048, heads=16, seq_len=1024, vocab=50304,
+                              batch=batch)
+    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=64 << 20, os_placement="cpu"), seed=0,
+                      hyper=K.AdamHyper(lr=1e-4), time_copies=True)
+    gen = torch.Generator().manual_seed(7)
+    toks = [torch.randint(0, schema.vocab, (batch, 1025), generator=gen).cuda() for _ in range(2)]
+    return tr, toks
+
+
+def timed_steps(tr, toks, steps):
+    for i in range(2):
+        tr.step(toks[i % 2])
+    tr.finish_host_work()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(steps):
+        tr.step(toks[i % 2])
+    tr.finish_host_work()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def timeline(tr, toks):
+    eng, ex = tr.sim.engine, tr.executor
+    marks = []
+    s0, f0 = eng.start_event, eng.finish_event
+
+    def start(ev):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append((ev.index, ev.name, "start", time.perf_counter(), e))
+        s0(ev)
+
+    def finish(ev):
+        f0(ev)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append((ev.index, ev.name, "finish", time.perf_counter(), e))
+
+    jobs = []
+    r0 = ex._run_host_adam
+
+    def run_host_adam(job, item, state):
+        t = time.perf_counter()
+        r0(job, item, state)
+        jobs.append((job.cids[0], t, time.perf_counter()))
+
+    for i in range(3):
+        tr.step(toks[i % 2])
+    tr.finish_host_work()
+    torch.cuda.synchronize()
+    eng.start_event, eng.finish_event, ex._run_host_adam = start, finish, run_host_adam
+    ex.stats.copy_events.clear()
+    z = torch.cuda.Event(enable_timing=True)
+    z.record()
+    hz = time.perf_counter()
+    tr.step(toks[0])
+    tr.step(toks[1])  # the next step's forward shows when the updated params land
+    tr.finish_host_work()
+    torch.cuda.synchronize()
+    eng.start_event, eng.finish_event, ex._run_host_adam = s0, f0, r0
+    ev = [(i, n, k, round((h - hz) * 1e3, 2), round(z.elapsed_time(e), 2))
+          for i, n, k, h, e in marks]
+    copies = [(name, round(z.elapsed_time(a), 2), round(z.elapsed_time(b), 2), nb)
+              for name, nb, a, b in ex.stats.copy_events]
+    host = [(cid, round((a - hz) * 1e3, 2), round((b - hz) * 1e3, 2)) for cid, a, b in jobs]
+    return {"events": ev, "copies": copies, "host_adam": host}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--ab", type=int, default=0)
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "offload_timeline.json"))
+    args = ap.parse_args()
+    if args.ab:
+        for rep in range(args.ab):
+            for early in ("1", "0"):
+                tr, toks = make(args.batch, {"CS_EARLY_DRAIN": early})
+                ms = timed_steps(tr, toks, 3)
+                print(json.dumps({"early_drain": early, "rep": rep, "ms_per_step": round(ms, 2),
+                                  "host_adam_s": round(tr.executor.stats.host_adam_seconds, 3)}),
+                      flush=True)
+                tr.close()
+                del tr, toks
+                torch.cuda.empty_cache()
+    tr, toks = make(args.batch, {"CS_EARLY_DRAIN": "1"})
+    res = timeline(tr, toks)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(res, f)
+    # compact view: GPU start of the FWD/BWD/ADAM phases of both steps
+    for i, n, k, h, g in res["events"]:
+        if n.startswith(("embedding", "adam", "l0.qkv", "l10.qkv", "l19.mlp_out")):
+            print("%-28s %-6s host %8.2f  gpu %8.2f" % (n, k, h, g))
+    print("copies:", len(res["copies"]), "host adam jobs:", len(res["host_adam"]))
+
+
+if __name__ == "__main__":
+    main()

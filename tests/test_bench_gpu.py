@@ -16,7 +16,7 @@ pytestmark = [pytest.mark.gpu,
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SMALL = ["--layers", "2", "--hidden", "256", "--heads", "4", "--seq", "128", "--vocab", "512",
          "--batch", "2", "--cap", str(1 << 18), "--steps", "3", "--warmup", "3",
-         "--no-cpu-baseline", "--no-offload-probe"]
+         "--no-cpu-baseline", "--no-offload-probe", "--no-c5"]
 
 
 def _line(out: str) -> dict:
@@ -49,6 +49,9 @@ def test_bench_two_ranks_gloo_same_device():
     cps = d["collectives_per_step"]
     assert cps["ledger_bytes_per_rank"] == cps["closed_form_bytes_per_rank"] > 0
     assert "collectives" in d
+    ins = d["collectives"]["in_step"]
+    assert ins["all_gather"]["per_step"] > 0 and ins["reduce_scatter_avg"]["per_step"] > 0
+    assert ins["all_gather"]["mean_ms"] > 0
 
 
 def test_library_loaded_before_torch_keeps_torch_cublas_working():

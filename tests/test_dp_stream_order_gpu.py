@@ -67,10 +67,11 @@ class StreamOrderedComm:
         work.wait()
         return None
 
-    def all_gather_slab(self, slab, async_op=False):
+    def all_gather_slab(self, slab, async_op=False, src=None):
         cap = slab.numel() // self.world
         self.calls.append(("all_gather", slab.numel() * slab.element_size()))
-        mine = slab[self.rank * cap:(self.rank + 1) * cap].cpu()  # after the slot's writes
+        mine = (slab[self.rank * cap:(self.rank + 1) * cap] if src is None
+                else src[:cap]).cpu()  # after the contribution's writes
         out = torch.empty(slab.numel(), dtype=slab.dtype)
         dist.all_gather_into_tensor(out, mine)
         return self._land(slab, out.pin_memory(), async_op)

@@ -309,7 +309,7 @@ def test_cpu_embedding_with_device_tokens():
     runs = []
     for dev in (False, True):
         tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
-                          dtype=torch.float16, seed=0)
+                          dtype=torch.float16, seed=0, untied_head=True)
         assert tr.host_embedding is not None
         if dev:
             runs.append([float(tr.step(t.cuda()).item()) for t in toks])
@@ -507,3 +507,32 @@ def test_unfused_model_trains_like_fused(place):
         out[fused] = ([tr.step_host(t) for t in toks], [_ledger(r)["transfers"] for r in tr.reports])
     assert out[True][1] == out[False][1]
     np.testing.assert_allclose(out[True][0], out[False][0], rtol=2e-3)
+
+
+def test_tied_model_under_a_cpu_embedding_plan_computes_it_on_the_gpu():
+    """The untied LM head is an explicit opt-in (the batch size must not
+    change the model): a tied model whose plan says CPU (C1) computes the
+    embedding on the GPU, warns, still produces the reference's ledgers, and
+    reports the embedding rows as billed but not realized."""
+    import warnings
+    case = "tiny_cap256Ki"
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        tr, schema = _trainer(case, untied_head=False)
+    assert any("untied LM head" in str(x.message) for x in w)
+    assert tr.sim.engine.embedding_device == "cpu" and tr.embedding_placement == "gpu"
+    assert tr.host_embedding is None and not tr.untied_head
+    ref = CASES[case]["ranks"]["0"]
+    for t in _tokens(schema, 3):
+        tr.step_host(t)
+    for mine, theirs in zip(tr.reports, ref["iterations"]):
+        assert _ledger(mine)["transfers"] == theirs["transfers"]
+    emb = sum(t.bytes for t in tr.reports[-1].transfers if t.chunk_id == "embedding")
+    assert emb > 0 and tr.ledger_rows_not_realized() == {"embedding": emb}
+    assert tr.gpu_resident_bytes == 14 * (schema.vocab + schema.seq_len) * schema.hidden_dim
+    import pytest as _pt
+    with _pt.raises(ValueError, match="untied"):
+        from paper_2108_05818_b200.trainer import ChunkTrainer
+        c = CASES[case]
+        ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                     embedding_placement="cpu")
