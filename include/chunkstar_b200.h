@@ -192,6 +192,15 @@ int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
                         const CsAdamHyper* hyper, const CsStepState* state,
                         int n_threads);
 
+/* Out-of-place host Adam: in[i] = (gradients in p16, p32, m, v) are read,
+ * out[i] = (p16, p32, m, v) receive the update (same bits as the in-place
+ * call), with non-temporal stores when out is 32-byte aligned.  For the
+ * speculative update of a CPU-placed position during the backward
+ * (engine.py:249-267 bill it at ADAM): if the step overflows the inputs are
+ * still intact.  in[i].n == out[i].n; state->skip must be 0. */
+int cs_adam_chunks_host_oop(const CsAdamItem* in, const CsAdamItem* out, int n_items, int dtype,
+                            const CsAdamHyper* hyper, const CsStepState* state, int n_threads);
+
 /* Host sum of squares (double accumulation) of fp16/bf16 gradients that sit
  * in host DRAM (grads of a chunk evicted to the CPU before the ADAM event,
  * or of CPU-placed positions); contributes to CsStepState.sumsq. */

@@ -124,6 +124,10 @@ SIGNATURES = {
     "cs_allreduce": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_void_p, ctypes.c_void_p]),
     "cs_comm_check": (ctypes.c_int, [ctypes.c_void_p]),
+    "cs_adam_chunks_host_oop": (ctypes.c_int, [ctypes.POINTER(CsAdamItem),
+                                               ctypes.POINTER(CsAdamItem), ctypes.c_int,
+                                               ctypes.c_int, ctypes.POINTER(CsAdamHyper),
+                                               ctypes.POINTER(CsStepState), ctypes.c_int]),
     "cs_comm_abort": (ctypes.c_int, [ctypes.c_void_p]),
 }
 

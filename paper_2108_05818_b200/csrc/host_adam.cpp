@@ -54,6 +54,75 @@ __attribute__((target("avx2,fma,f16c"))) inline void store16(uint16_t* p, __m256
   _mm_storeu_si128(reinterpret_cast<__m128i*>(p), h);
 }
 
+// in: g16 (gradients), p32, m, v; out: o16, o32, om, ov (may alias the inputs
+// unless STREAM; STREAM needs 32-byte aligned fp32 and 16-byte aligned fp16 outputs)
+template <int DT, bool STREAM = false>
+__attribute__((target("avx2,fma,f16c"))) inline void adam8_oop(
+    const uint16_t* g16, const float* p32, const float* m, const float* v, uint16_t* o16,
+    float* o32, float* om, float* ov, const Consts& c) {
+  __m256 g = _mm256_mul_ps(load16<DT>(g16), c.gs);
+  __m256 p = _mm256_loadu_ps(p32);
+  if (c.has_wd) {
+    if (c.adamw) p = _mm256_mul_ps(p, c.decay);
+    else g = _mm256_fmadd_ps(c.wd, p, g);
+  }
+  const __m256 m0 = _mm256_loadu_ps(m);
+  const __m256 mm = _mm256_fmadd_ps(c.c1, _mm256_sub_ps(g, m0), m0);
+  const __m256 vv = _mm256_fmadd_ps(_mm256_mul_ps(c.c2, g), g,
+                                    _mm256_mul_ps(_mm256_loadu_ps(v), c.b2));
+  const __m256 denom = _mm256_add_ps(_mm256_div_ps(_mm256_sqrt_ps(vv), c.sb), c.eps);
+  p = _mm256_add_ps(p, _mm256_div_ps(_mm256_mul_ps(c.nss, mm), denom));
+  if (STREAM) {  // fresh output lines: non-temporal stores skip the read-for-ownership
+    _mm256_stream_ps(o32, p);
+    _mm256_stream_ps(om, mm);
+    _mm256_stream_ps(ov, vv);
+    alignas(16) uint16_t h[8];
+    store16<DT>(h, p);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(o16),
+                     _mm_load_si128(reinterpret_cast<const __m128i*>(h)));
+  } else {
+    _mm256_storeu_ps(o32, p);
+    _mm256_storeu_ps(om, mm);
+    _mm256_storeu_ps(ov, vv);
+    store16<DT>(o16, p);
+  }
+}
+
+template <int DT>
+__attribute__((target("avx2,fma,f16c"))) void adam_range_oop(const CsAdamItem& in,
+                                                          const CsAdamItem& out, int64_t lo,
+                                                          int64_t hi, const Consts& c) {
+  const uint16_t* g16 = static_cast<const uint16_t*>(in.p16);
+  uint16_t* o16 = static_cast<uint16_t*>(out.p16);
+  int64_t e = lo;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(out.p32) | reinterpret_cast<uintptr_t>(out.m) |
+                         reinterpret_cast<uintptr_t>(out.v)) & 31) == 0 &&
+                       (reinterpret_cast<uintptr_t>(o16) & 15) == 0 && (lo & 7) == 0;
+  if (aligned) {
+    for (; e + 8 <= hi; e += 8)
+      adam8_oop<DT, true>(g16 + e, in.p32 + e, in.m + e, in.v + e, o16 + e, out.p32 + e,
+                          out.m + e, out.v + e, c);
+  } else {
+    for (; e + 8 <= hi; e += 8)
+      adam8_oop<DT>(g16 + e, in.p32 + e, in.m + e, in.v + e, o16 + e, out.p32 + e, out.m + e,
+                    out.v + e, c);
+  }
+  if (e < hi) {  // tail: the same 8-lane code on a padded copy
+    alignas(32) uint16_t t16[8] = {0};
+    alignas(32) float tp[8] = {0}, tm[8] = {0}, tv[8] = {0};
+    const int64_t k = hi - e;
+    std::memcpy(t16, g16 + e, k * 2);
+    std::memcpy(tp, in.p32 + e, k * 4);
+    std::memcpy(tm, in.m + e, k * 4);
+    std::memcpy(tv, in.v + e, k * 4);
+    adam8_oop<DT>(t16, tp, tm, tv, t16, tp, tm, tv, c);
+    std::memcpy(o16 + e, t16, k * 2);
+    std::memcpy(out.p32 + e, tp, k * 4);
+    std::memcpy(out.m + e, tm, k * 4);
+    std::memcpy(out.v + e, tv, k * 4);
+  }
+}
+
 template <int DT>
 __attribute__((target("avx2,fma,f16c"))) inline void adam8(uint16_t* p16, float* p32, float* m,
                                                         float* v, const Consts& c) {
@@ -174,6 +243,49 @@ extern "C" int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dty
     const int64_t hi = lo + kRange < it.n ? lo + kRange : it.n;
     if (dtype == CS_FP16) adam_range<CS_FP16>(it, lo, hi, c);
     else adam_range<CS_BF16>(it, lo, hi, c);
+  }
+  return 0;
+}
+
+extern "C" int cs_adam_chunks_host_oop(const CsAdamItem* in, const CsAdamItem* out,
+                                       int n_items, int dtype, const CsAdamHyper* hyper,
+                                       const CsStepState* state, int n_threads) {
+  if (n_items < 0 || (n_items > 0 && (!in || !out)) || !hyper || !state ||
+      (dtype != CS_FP16 && dtype != CS_BF16) || state->skip) {
+    cs::set_error("cs_adam_chunks_host_oop: invalid argument (a skipped step has no update)");
+    return CS_EINVAL;
+  }
+  if (!__builtin_cpu_supports("avx2") || !__builtin_cpu_supports("fma") ||
+      !__builtin_cpu_supports("f16c")) {
+    cs::set_error("cs_adam_chunks_host_oop: host CPU lacks AVX2/FMA/F16C");
+    return CS_EINVAL;
+  }
+  const Consts c = make_consts(*hyper, *state);
+  constexpr int64_t kRange = 1 << 16;
+  std::vector<std::pair<int, int64_t>> ranges;
+  for (int i = 0; i < n_items; ++i) {
+    const CsAdamItem& a = in[i];
+    const CsAdamItem& b = out[i];
+    if (a.n < 0 || a.n != b.n ||
+        (a.n > 0 && (!a.p16 || !a.p32 || !a.m || !a.v || !b.p16 || !b.p32 || !b.m || !b.v))) {
+      cs::set_error("cs_adam_chunks_host_oop: item %d invalid", i);
+      return CS_EINVAL;
+    }
+    for (int64_t lo = 0; lo < a.n; lo += kRange) ranges.emplace_back(i, lo);
+  }
+  const int64_t nr = (int64_t)ranges.size();
+  const int threads = cs::host_threads(n_threads);
+#pragma omp parallel num_threads(threads)
+  {
+#pragma omp for schedule(static)
+    for (int64_t r = 0; r < nr; ++r) {
+      const int i = ranges[r].first;
+      const int64_t lo = ranges[r].second;
+      const int64_t hi = lo + kRange < in[i].n ? lo + kRange : in[i].n;
+      if (dtype == CS_FP16) adam_range_oop<CS_FP16>(in[i], out[i], lo, hi, c);
+      else adam_range_oop<CS_BF16>(in[i], out[i], lo, hi, c);
+    }
+    _mm_sfence();  // each thread's non-temporal stores are visible before the join
   }
   return 0;
 }

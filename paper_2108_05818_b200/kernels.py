@@ -136,6 +136,56 @@ def adam_chunks_host(items, hyper: AdamHyper, state: N.CsStepState, n_threads: i
             "cs_adam_chunks_host")
 
 
+def speculate_step_scalars(prev: N.CsStepState, hyper: AdamHyper) -> N.CsStepState:
+    """The step scalars ``cs_adam_prepare`` will produce for the NEXT step if
+    its gradients are finite and not clipped, from the state it left after
+    this one (same IEEE operations, so the same bits): grad_scale = 1 / loss
+    scale, step + 1, beta powers, step_size, sqrt_bc2, skip = 0.  Only the
+    fields the Adam reads are meaningful."""
+    import numpy as np
+    s = N.CsStepState.from_buffer_copy(bytes(prev))
+    b1p = float(np.float64(prev.beta1_pow) * np.float64(hyper.betas[0]))
+    b2p = float(np.float64(prev.beta2_pow) * np.float64(hyper.betas[1]))
+    s.grad_scale = float(np.float32(1.0) / np.float32(prev.loss_scale))
+    s.step = prev.step + 1
+    s.beta1_pow, s.beta2_pow = b1p, b2p
+    s.step_size = float(np.float32(np.float64(hyper.lr) / (np.float64(1.0) - np.float64(b1p))))
+    s.sqrt_bc2 = float(np.float32(np.sqrt(np.float64(1.0) - np.float64(b2p))))
+    s.skip = 0
+    return s
+
+
+def same_update_scalars(a: N.CsStepState, b: N.CsStepState) -> bool:
+    """True when two states drive the Adam identically (the fields it reads)."""
+    import numpy as np
+    f32 = lambda x: np.float32(x).tobytes()  # noqa: E731
+    return (a.skip == b.skip == 0 and f32(a.grad_scale) == f32(b.grad_scale)
+            and f32(a.step_size) == f32(b.step_size) and f32(a.sqrt_bc2) == f32(b.sqrt_bc2))
+
+
+def adam_chunks_host_oop(items_in, items_out, hyper: AdamHyper, state: N.CsStepState,
+                         n_threads: int = 0) -> None:
+    """Out-of-place host Adam (cs_adam_chunks_host_oop): reads (g16, p32, m, v)
+    of items_in, writes (p16, p32, m, v) of items_out; same bits as
+    :func:`adam_chunks_host`."""
+    if not items_in:
+        return
+    if len(items_in) != len(items_out):
+        raise ValueError("adam_chunks_host_oop: in / out item counts differ")
+    a = (N.CsAdamItem * len(items_in))()
+    b = (N.CsAdamItem * len(items_in))()
+    dt = _code(items_in[0][0].dtype)
+    for i, (x, y) in enumerate(zip(items_in, items_out)):
+        if any(t.is_cuda for t in x[:4] + y[:4]):
+            raise ValueError("host adam needs host tensors")
+        a[i] = N.CsAdamItem(*(t.data_ptr() for t in x[:4]), x[4])
+        b[i] = N.CsAdamItem(*(t.data_ptr() for t in y[:4]), y[4])
+    h = hyper.c()
+    N.check(N.load().cs_adam_chunks_host_oop(a, b, len(items_in), dt, ctypes.byref(h),
+                                             ctypes.byref(state), int(n_threads)),
+            "cs_adam_chunks_host_oop")
+
+
 def grad_sumsq_host(grads: Sequence[Tuple[torch.Tensor, int]], n_threads: int = 0) -> float:
     """Sum of squares of host-resident fp16/bf16 gradients (double)."""
     if not grads:

@@ -37,10 +37,11 @@ allocator, compute-stream pool), host payloads come from its pinned caching
 host allocator.
 """
 
+import heapq
 import os
 import threading
 import time
-from concurrent.futures import Future, ThreadPoolExecutor
+from concurrent.futures import Future
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Set, Tuple
 
@@ -101,6 +102,54 @@ class ChunkComm:
         dist.all_reduce(t, op=dist.ReduceOp.AVG, group=self.group)
 
 
+class _PriorityWorker:
+    """One host thread running host-Adam jobs lowest position first.
+
+    Jobs of CPU-placed positions are submitted in two orders: speculative
+    updates during the backward, as each position's gradients become final
+    (highest position first: the backward walks the layers in reverse), and
+    the ADAM walk's in-place updates and settles (ascending).  The next
+    forward needs the lowest positions first, so whatever is queued runs in
+    ascending position order; a job already running is not preempted.
+    Futures follow concurrent.futures semantics (``cancel()`` succeeds while
+    the job is still queued)."""
+
+    def __init__(self):
+        self._heap: List[tuple] = []
+        self._cv = threading.Condition()
+        self._seq = 0
+        self._thread = threading.Thread(target=self._loop, name="cs-host-adam", daemon=True)
+        self._thread.start()
+
+    def submit(self, priority: int, fn, *args) -> Future:
+        fut: Future = Future()
+        with self._cv:
+            heapq.heappush(self._heap, (priority, self._seq, fut, fn, args))
+            self._seq += 1
+            self._cv.notify()
+        return fut
+
+    def _loop(self) -> None:
+        while True:
+            with self._cv:
+                while not self._heap:
+                    self._cv.wait()
+                _, _, fut, fn, args = heapq.heappop(self._heap)
+            if fn is None:
+                return
+            if not fut.set_running_or_notify_cancel():
+                continue
+            try:
+                fut.set_result(fn(*args))
+            except BaseException as e:  # delivered to whoever joins the job
+                fut.set_exception(e)
+
+    def shutdown(self) -> None:
+        with self._cv:
+            heapq.heappush(self._heap, (float("inf"), self._seq, Future(), None, ()))
+            self._cv.notify()
+
+
 class _HostAdamJob:
     """One CPU-placed position's host Adam, run by the executor's worker
     thread; the param chunk's ``adam_copy`` H2D (`engine.py:265-267`) is
@@ -111,7 +160,7 @@ class _HostAdamJob:
         self.cids = tuple(cids)
         self.lock = threading.Lock()
         self.adam_done = False
-        self.h2d = None            # deferred (chunk, src tensor, dst tensor, prior event)
+        self.h2d = None            # deferred (chunk id, dst tensor, prior event)
         self.future: Optional[Future] = None
 
 
@@ -132,6 +181,10 @@ class ExecStats:
     gather_prefetch_issued: int = 0
     gather_prefetch_hits: int = 0
     host_adam_seconds: float = 0.0
+    spec_issued: int = 0
+    spec_committed: int = 0
+    spec_discarded: int = 0
+    spec_cancelled: int = 0
     copy_events: List[Tuple[str, int, "torch.cuda.Event", "torch.cuda.Event"]] = field(
         default_factory=list)
 
@@ -192,7 +245,25 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         #: (the host Adam slows down by what it overlaps).  CS_ASYNC_HOST_ADAM=0
         #: restores the synchronous walk.
         self.async_host_adam = os.environ.get("CS_ASYNC_HOST_ADAM", "1") != "0"
-        self._worker: Optional[ThreadPoolExecutor] = None
+        self._worker: Optional[_PriorityWorker] = None
+        #: speculative host Adam: once a CPU-placed position's gradients are
+        #: final and drained (see ``early_drain``) its update starts on the
+        #: worker during the rest of the backward, out of place into shadow
+        #: buffers (cs_adam_chunks_host_oop), with the step scalars
+        #: cs_adam_prepare will produce if the step is finite and unclipped
+        #: (``kernels.speculate_step_scalars``, bit-exact).  At the position's
+        #: ADAM turn a settle job (same priority) adopts the shadows if the real
+        #: scalars are those bits (pointer swap), else runs the normal update
+        #: from the intact inputs; an update not started yet is cancelled and
+        #: replaced by the normal one.  Bit-identical to the non-speculative
+        #: walk; off when gradients are clipped (the coefficient needs every
+        #: gradient).  Shadow buffers are bounded by ``spec_budget_bytes``.
+        self.speculative_host_adam = os.environ.get("CS_SPEC_HOST_ADAM", "1") != "0"
+        self.spec_budget_bytes = int(float(os.environ.get("CS_SPEC_HOST_GB", "16")) * 2**30)
+        self._spec: Dict[int, tuple] = {}        # position -> (future, d, ins, shadow)
+        self._spec_free: List[tuple] = []        # recycled (p16, p32, m, v) host buffers
+        self._spec_bytes = 0                     # pinned bytes held by shadow sets
+        self._spec_state = None
         self._jobs: Dict[int, _HostAdamJob] = {}   # chunk id -> unfinished job
         #: drain a host-placed position's gradients D2H as soon as they are
         #: final (after its last BWD op; at p > 1 after its reduce-scatter),
@@ -369,34 +440,39 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         go H2D as soon as the update finishes (from the worker); False if it
         already finished (the caller copies now)."""
         cid = chunk.chunk_id
-        s = self.payload[CPU][cid]
         d = self._alloc_for_copy(chunk)
         prior = self.ready.pop((cid, CPU), None)
         with job.lock:
             if job.adam_done:
                 self._jobs.pop(cid, None)
-                done = self._transfer(s, d, CPU, GPU, prior)
+                done = self._transfer(self.payload[CPU][cid], d, CPU, GPU, prior)
                 if done is not None:
                     self.ready[(cid, GPU)] = done
                 self.payload[GPU][cid] = d
                 return True
-            job.h2d = (cid, s, d, prior)
+            # the source is looked up when the job is done: a settled
+            # speculative update swaps in its shadow buffer
+            job.h2d = (cid, d, prior)
         self.payload[GPU][cid] = d
         return True
+
+    def _job_done(self, job: _HostAdamJob) -> None:
+        """The host update of ``job`` is complete: issue its deferred H2D."""
+        with job.lock:
+            job.adam_done = True
+            h2d = job.h2d
+            if h2d is not None:
+                cid, d, prior = h2d
+                done = self._transfer(self.payload[CPU][cid], d, CPU, GPU, prior)
+                if done is not None:
+                    self.ready[(cid, GPU)] = done
 
     def _run_host_adam(self, job: _HostAdamJob, item, state) -> None:
         t0 = time.perf_counter()
         K.adam_chunks_host([item], self.hyper, state, self.host_threads)
         with self._stats_lock:
             self.stats.host_adam_seconds += time.perf_counter() - t0
-        with job.lock:
-            job.adam_done = True
-            h2d = job.h2d
-            if h2d is not None:
-                cid, s, d, prior = h2d
-                done = self._transfer(s, d, CPU, GPU, prior)
-                if done is not None:
-                    self.ready[(cid, GPU)] = done
+        self._job_done(job)
 
     def _transfer(self, s: torch.Tensor, d: torch.Tensor, src: str, dst: str,
                   prior: Optional["torch.cuda.Event"], after=None):
@@ -496,7 +572,75 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                                   self.ready.get((cid, GPU)), after=self._coll_work.get(cid))
             self._predrained[cid] = (d, done)
             self.stats.early_drains += 1
+            self._speculate(pos, chunk, d, done)
         self._drain_candidates = keep
+
+    # -- speculative host Adam (see ``speculative_host_adam``) ----------------------
+
+    def _speculate(self, pos: int, chunk: Chunk, d: torch.Tensor, drained) -> None:
+        if (not self.speculative_host_adam or not self.async_host_adam
+                or self.max_grad_norm > 0 or self._state_snap is None or pos in self._spec):
+            return
+        triplet = self.chunk_set.os_triplet(pos)
+        if any(not self.has(c, CPU) or c.chunk_id in self._jobs for c in triplet) \
+                or chunk.chunk_id in self._jobs:
+            return
+        shadow = self._take_shadow(chunk, triplet)
+        if shadow is None:
+            return
+        if self._spec_state is None:
+            self._spec_state = K.speculate_step_scalars(
+                K.StepState.from_snapshot(self._state_snap), self.hyper)
+        n = chunk.used_elems
+        ins = (d,) + tuple(self.payload[CPU][c.chunk_id] for c in triplet)
+        waits = [drained] + [self.ready[(c.chunk_id, CPU)] for c in triplet
+                             if (c.chunk_id, CPU) in self.ready]
+        if self._worker is None:
+            self._worker = _PriorityWorker()
+        fut = self._worker.submit(pos, self._run_spec, waits, ins + (n,), shadow + (n,),
+                                  self._spec_state)
+        self._spec[pos] = (fut, ins, shadow, self._spec_state)
+        self.stats.spec_issued += 1
+
+    def _take_shadow(self, chunk: Chunk, triplet) -> Optional[tuple]:
+        if self._spec_free:
+            return self._spec_free.pop()
+        nbytes = chunk.capacity_elems * (2 + 12)
+        if self._spec_bytes + nbytes > self.spec_budget_bytes:
+            return None
+        self._spec_bytes += nbytes
+        return tuple(self._alloc(c, CPU) for c in (chunk,) + tuple(triplet))
+
+    def _run_spec(self, waits, item_in, item_out, state) -> None:
+        for ev in waits:
+            ev.synchronize()
+        t0 = time.perf_counter()
+        K.adam_chunks_host_oop([item_in], [item_out], self.hyper, state, self.host_threads)
+        with self._stats_lock:
+            self.stats.host_adam_seconds += time.perf_counter() - t0
+
+    def _settle_spec(self, job: _HostAdamJob, spec, param: Chunk, triplet, state) -> None:
+        """At the position's ADAM turn, on the worker: adopt the speculative
+        update if it used this step's real scalars and the current payloads,
+        else run the normal update from the (intact) inputs."""
+        fut, ins, shadow, spec_state = spec
+        fut.result()
+        cpu = self.payload[CPU]
+        cids = (param.chunk_id,) + tuple(c.chunk_id for c in triplet)
+        ok = (K.same_update_scalars(spec_state, state)
+              and all(cpu.get(cid) is t for cid, t in zip(cids, ins)))
+        if ok:
+            for cid, t in zip(cids, shadow):
+                cpu[cid] = t
+            self._spec_free.append(ins)
+            with self._stats_lock:
+                self.stats.spec_committed += 1
+            self._job_done(job)
+            return
+        self._spec_free.append(shadow)
+        with self._stats_lock:
+            self.stats.spec_discarded += 1
+        self._run_host_adam(job, tuple(cpu[cid] for cid in cids) + (param.used_elems,), state)
 
     def before_event(self, ev, iteration: int) -> None:
         self._cur_event = ev.index
@@ -851,21 +995,34 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self._host_state = self._step_scalars_on_host()
         for c in (param,) + triplet:
             self.wait_ready(c, CPU)
+        self.stats.host_adam_items += 1
+        spec = self._spec.pop(position, None)
+        if spec is not None and spec[0].cancel():  # not started: the normal update instead
+            self._spec_free.append(spec[2])
+            self.stats.spec_cancelled += 1
+            spec = None
+        if spec is not None:
+            job = _HostAdamJob(c.chunk_id for c in (param,) + triplet)
+            for cid in job.cids:
+                self._jobs[cid] = job
+            job.future = self._worker.submit(position, self._settle_spec, job, spec, param,
+                                             triplet, self._host_state)
+            return
         p16 = self.tensor(param, CPU)
         p32, m, v = (self.tensor(c, CPU) for c in triplet)
         item = (p16, p32, m, v, n)
-        self.stats.host_adam_items += 1
         if not self.async_host_adam:
             t0 = time.perf_counter()
             K.adam_chunks_host([item], self.hyper, self._host_state, self.host_threads)
             self.stats.host_adam_seconds += time.perf_counter() - t0
             return
         if self._worker is None:
-            self._worker = ThreadPoolExecutor(max_workers=1, thread_name_prefix="cs-host-adam")
+            self._worker = _PriorityWorker()
         job = _HostAdamJob(c.chunk_id for c in (param,) + triplet)
         for cid in job.cids:
             self._jobs[cid] = job
-        job.future = self._worker.submit(self._run_host_adam, job, item, self._host_state)
+        job.future = self._worker.submit(position, self._run_host_adam, job, item,
+                                         self._host_state)
 
     def retain_param_payload(self, chunk: Chunk, device: str) -> None:
         self._retain_req.add((chunk.chunk_id, device))
@@ -913,6 +1070,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 self.stats.host_adam_seconds += dt
             he.host_seconds += dt
             he.grads_ready = False
+        for pos in list(self._spec):  # never reached its ADAM turn: recycle
+            fut, _, shadow, _ = self._spec.pop(pos)
+            if not fut.cancel():
+                fut.result()
+            self._spec_free.append(shadow)
+            self.stats.spec_discarded += 1
+        self._spec_state = None
         self._drain_candidates = []
         self._rs_out.clear()
         self._retain_req.clear()

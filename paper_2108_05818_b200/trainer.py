@@ -103,7 +103,8 @@ class ChunkTrainer:
                  gather_depth: int = 2, embedding_placement: str = "plan",
                  untied_head: bool = False,
                  async_host_adam: Optional[bool] = None,
-                 comm=None, bind_host: Optional[bool] = None):
+                 comm=None, bind_host: Optional[bool] = None,
+                 speculative_host_adam: Optional[bool] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -187,6 +188,8 @@ class ChunkTrainer:
         ex = self.executor
         if async_host_adam is not None:
             ex.async_host_adam = async_host_adam
+        if speculative_host_adam is not None:
+            ex.speculative_host_adam = speculative_host_adam
         self.tracer = None
         if non_model == "measured" and non_model_fn is None:
             from .tracer import MemoryTracer

@@ -106,17 +106,22 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "offload_timeline.json"))
     args = ap.parse_args()
     if args.ab:
+        arms = [{"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1"},
+                {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "0"},
+                {"CS_EARLY_DRAIN": "0", "CS_SPEC_HOST_ADAM": "0"}]
         for rep in range(args.ab):
-            for early in ("1", "0"):
-                tr, toks = make(args.batch, {"CS_EARLY_DRAIN": early})
+            for env in arms:
+                tr, toks = make(args.batch, env)
                 ms = timed_steps(tr, toks, 3)
-                print(json.dumps({"early_drain": early, "rep": rep, "ms_per_step": round(ms, 2),
-                                  "host_adam_s": round(tr.executor.stats.host_adam_seconds, 3)}),
-                      flush=True)
+                st = tr.executor.stats
+                print(json.dumps({"env": env, "rep": rep, "ms_per_step": round(ms, 2),
+                                  "host_adam_s": round(st.host_adam_seconds, 3),
+                                  "spec": [st.spec_issued, st.spec_committed, st.spec_discarded,
+                                           st.spec_cancelled]}), flush=True)
                 tr.close()
                 del tr, toks
                 torch.cuda.empty_cache()
-    tr, toks = make(args.batch, {"CS_EARLY_DRAIN": "1"})
+    tr, toks = make(args.batch, {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1"})
     res = timeline(tr, toks)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:

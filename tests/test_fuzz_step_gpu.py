@@ -18,7 +18,7 @@ evicts).  Properties checked on every configuration:
 * every K1 launch of the tight-budget run equals the C oracle byte for byte
   (random lr, betas, weight decay, Adam / AdamW);
 * numerics: the tight-budget run — with a random embedding placement
-  (plan / host / device operator), synchronous or asynchronous
+  (plan / host / device operator), synchronous, asynchronous or speculative
   host Adam —
   is bit-identical to an all-resident run of the same model (deterministic
   attention backend).
@@ -54,6 +54,7 @@ def _config(seed):
     dtype = r.choice([torch.float16, torch.bfloat16])
     run = dict(embedding_placement=r.choice(["plan", "cpu", "gpu"]),
                async_host_adam=r.random() < 0.5)
+    run["speculative_host_adam"] = run["async_host_adam"] and r.random() < 0.7
     wd = r.choice([0.0, 0.0, 0.01, 0.1])
     hyper = dict(lr=r.choice([1e-4, 1e-3]), betas=r.choice([(0.9, 0.999), (0.9, 0.95)]),
                  weight_decay=wd, adamw=wd > 0 and r.random() < 0.5)

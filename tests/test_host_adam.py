@@ -114,3 +114,61 @@ def test_host_threads_share_of_the_affinity_mask(native_lib):
         out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True,
                              text=True, check=True).stdout.split()
         assert [int(x) for x in out] == [max(want, 1), 5], (env, out)
+
+
+def test_out_of_place_host_adam_equals_in_place(native_lib):
+    """cs_adam_chunks_host_oop: same bits as the in-place update, inputs intact."""
+    rng = np.random.default_rng(9)
+    hyper = K.AdamHyper(lr=1e-3, betas=(0.9, 0.95), weight_decay=0.01, adamw=True)
+    st = N.CsStepState()
+    st.grad_scale, st.step_size, st.sqrt_bc2, st.skip = 0.125, 1e-3, 0.3, 0
+    for dtype in (torch.float16, torch.bfloat16):
+        for n in (1, 9, 65536 + 5):
+            g = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(dtype)
+            p, m = (torch.from_numpy(rng.standard_normal(n).astype(np.float32) * 0.02)
+                    for _ in range(2))
+            v = torch.from_numpy(np.abs(rng.standard_normal(n)).astype(np.float32) * 1e-6)
+            ins = [t.clone() for t in (g, p, m, v)]
+            outs = [torch.empty_like(t) for t in ins]
+            K.adam_chunks_host_oop([(*ins, n)], [(*outs, n)], hyper, st, n_threads=3)
+            for a, b in zip(ins, (g, p, m, v)):      # inputs untouched
+                assert torch.equal(a, b)
+            K.adam_chunks_host([(g, p, m, v, n)], hyper, st, n_threads=2)
+            for a, b in zip(outs, (g, p, m, v)):     # outputs == in-place result
+                assert torch.equal(a.view(torch.int16 if a.dtype != torch.float32
+                                          else torch.int32),
+                                   b.view(torch.int16 if b.dtype != torch.float32
+                                          else torch.int32))
+    st.skip = 1
+    with pytest.raises(N.NativeError):
+        K.adam_chunks_host_oop([(*ins, n)], [(*outs, n)], hyper, st)
+
+
+def test_speculated_step_scalars_match_prepare(oracle_lib):
+    """kernels.speculate_step_scalars reproduces cs_adam_prepare (the oracle's
+    restatement, pinned to the device kernel by tests/test_kernels_gpu.py)
+    bit for bit for finite, unclipped steps — through loss-scale growth."""
+    O = oracle_lib
+    for lr, b1, b2 in ((1e-4, 0.9, 0.999), (3e-3, 0.8, 0.95)):
+        hyper = K.AdamHyper(lr=lr, betas=(b1, b2))
+        s = O.step_state(65536.0)
+        for step in range(40):
+            prev = N.CsStepState()
+            for f, _ in N.CsStepState._fields_:
+                setattr(prev, f, getattr(s, f))
+            s.sumsq = 1.0 + step
+            O.adam_prepare(s, lr, b1, b2, growth=2.0, backoff=0.5, interval=7, dynamic=True)
+            real = N.CsStepState()
+            for f, _ in N.CsStepState._fields_:
+                setattr(real, f, getattr(s, f))
+            spec = K.speculate_step_scalars(prev, hyper)
+            assert K.same_update_scalars(spec, real), (lr, step)
+            assert spec.step == real.step
+        # an overflowing step is never matched (its update is a skip)
+        prev = real
+        s.sumsq = float("inf")
+        O.adam_prepare(s, lr, b1, b2, dynamic=True)
+        real = N.CsStepState()
+        for f, _ in N.CsStepState._fields_:
+            setattr(real, f, getattr(s, f))
+        assert not K.same_update_scalars(K.speculate_step_scalars(prev, hyper), real)

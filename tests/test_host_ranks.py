@@ -1,0 +1,115 @@
+"""Per-rank host resources for one-process-per-GPU runs (no GPU needed).
+
+torchrun exports OMP_NUM_THREADS=1 and LOCAL_WORLD_SIZE; each rank must
+still give its host kernels (host Adam of CPU-placed optimizer triplets,
+the CPU-placed embedding) its share of the host cores — not one thread, not
+the whole machine.  Two ranks launched by torchrun (gloo) each bind to half
+of the cores (hostres.bind_local_rank, as ChunkTrainer does when
+LOCAL_WORLD_SIZE > 1), get cs_host_threads(0) == that half, and run the host
+Adam concurrently; each rank's per-thread rate is compared with a single
+process's per-thread rate on all cores.
+"""
+
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r"""
+import json, os, sys, time
+sys.path.insert(0, %(root)r)
+import torch
+import torch.distributed as dist
+from paper_2108_05818_b200 import hostres, kernels as K, _native as N
+
+def rate(n, threads):
+    g = torch.zeros(n, dtype=torch.float16); p = torch.randn(n) * 0.02
+    m = torch.zeros(n); v = torch.zeros(n)
+    st = N.CsStepState(); st.grad_scale, st.step_size, st.sqrt_bc2 = 1.0, 1e-4, 0.03
+    h = K.AdamHyper()
+    K.adam_chunks_host([(g, p, m, v, n)], h, st, threads)
+    best = 1e9
+    for _ in range(3):
+        t = time.perf_counter(); K.adam_chunks_host([(g, p, m, v, n)], h, st, threads)
+        best = min(best, time.perf_counter() - t)
+    return n / best / 1e9
+
+dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
+local_rank, local_world = int(os.environ["LOCAL_RANK"]), int(os.environ["LOCAL_WORLD_SIZE"])
+before = len(os.sched_getaffinity(0))
+info = hostres.bind_local_rank(local_rank, local_world, local_rank)
+threads = hostres.host_threads(0)
+dist.barrier()
+r = rate(1 << 24, threads)
+out = {"rank": rank, "omp_env": os.environ.get("OMP_NUM_THREADS"), "before": before,
+       "cpus": sorted(os.sched_getaffinity(0)), "threads": threads, "gelem_s": r, "info": info}
+objs = [None] * world
+dist.all_gather_object(objs, out)
+if rank == 0:
+    with open(%(out)r, "w") as f:
+        json.dump(objs, f)
+dist.destroy_process_group()
+"""
+
+SINGLE = r"""
+import json, os, sys, time
+sys.path.insert(0, %(root)r)
+import torch
+from paper_2108_05818_b200 import hostres, kernels as K, _native as N
+n = 1 << 24
+g = torch.zeros(n, dtype=torch.float16); p = torch.randn(n) * 0.02
+m = torch.zeros(n); v = torch.zeros(n)
+st = N.CsStepState(); st.grad_scale, st.step_size, st.sqrt_bc2 = 1.0, 1e-4, 0.03
+h = K.AdamHyper(); threads = hostres.host_threads(0)
+K.adam_chunks_host([(g, p, m, v, n)], h, st, threads)
+best = 1e9
+for _ in range(3):
+    t = time.perf_counter(); K.adam_chunks_host([(g, p, m, v, n)], h, st, threads)
+    best = min(best, time.perf_counter() - t)
+print(json.dumps({"threads": threads, "gelem_s": n / best / 1e9}))
+"""
+
+
+@pytest.mark.skipif(len(os.sched_getaffinity(0)) < 2, reason="needs >= 2 cores")
+def test_two_local_ranks_split_the_host_cores():
+    cores = len(os.sched_getaffinity(0))
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "ranks.json")
+        script = os.path.join(d, "w.py")
+        with open(script, "w") as f:
+            f.write(WORKER % {"root": ROOT, "out": out})
+        env = dict(os.environ)
+        env.pop("CS_HOST_BOUND", None)
+        env.pop("OMP_NUM_THREADS", None)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+               "--master-port", str(29700 + os.getpid() % 200), script]
+        res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, (res.stdout + res.stderr)[-3000:]
+        with open(out) as f:
+            ranks = json.load(f)
+        env1 = dict(env, LOCAL_WORLD_SIZE="1")
+        single = subprocess.run([sys.executable, "-c", SINGLE % {"root": ROOT}], env=env1,
+                                capture_output=True, text=True, timeout=600, check=True)
+        one = json.loads(single.stdout.strip().splitlines()[-1])
+    assert one["threads"] == cores
+    a, b = ranks
+    assert a["omp_env"] == b["omp_env"] == "1"          # torchrun's default
+    assert a["info"]["bound"] and b["info"]["bound"]
+    assert a["threads"] == len(a["cpus"]) == cores // 2  # not 1, not all cores
+    assert b["threads"] == len(b["cpus"]) == cores - cores // 2
+    assert not set(a["cpus"]) & set(b["cpus"])          # disjoint shares
+    per_thread_single = one["gelem_s"] / one["threads"]
+    for r in ranks:
+        # memory-bound host Adam: each rank's per-thread rate stays close to a
+        # lone process's (ratio recorded in the failure message)
+        ratio = (r["gelem_s"] / r["threads"]) / per_thread_single
+        print("rank %d: %d threads %.3f Gelem/s, per-thread ratio vs lone process %.2f"
+              % (r["rank"], r["threads"], r["gelem_s"], ratio))
+        assert ratio >= 0.8, (ratio, r, one)

@@ -188,6 +188,43 @@ def test_lagged_loss_reads_match_synchronous_steps(case, graph):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
 
+@pytest.mark.parametrize("case,init_scale", [("tiny_os_cpu", None), ("tiny_tight", None),
+                                              ("tiny_os_cpu", 2.0 ** 40)])
+def test_speculative_host_adam_is_bit_identical(case, init_scale):
+    """Speculative host Adam (updates of host-placed positions started during
+    the backward on the priority worker, settled at ADAM: adopted only if the
+    real step scalars match, else recomputed) gives the same ledgers, losses
+    and parameters as the normal walk; an overflowing start (scale 2^40)
+    exercises the discard path."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES[case]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 6)
+    out = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for spec in (False, True):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0, speculative_host_adam=spec,
+                              init_loss_scale=init_scale, untied_head=True)
+            tr.executor.copy_delay_cycles = 500_000 if spec else 0  # moves land late too
+            losses = [tr.step_host(t) for t in toks]
+            tr.finish_host_work()
+            params = [tr.local_chunk_payload(p).cpu().clone()
+                      for p in range(tr.sim.chunk_set.positions)]
+            out[spec] = (losses, params, [_ledger(r) for r in tr.reports], tr.executor.stats)
+    st = out[True][3]
+    assert st.spec_issued > 0 and out[False][3].spec_issued == 0
+    if init_scale is None:
+        assert st.spec_committed > 0 and st.spec_discarded == 0
+    else:  # overflow steps: speculation thrown away (or cancelled before it ran)
+        assert st.spec_discarded + st.spec_cancelled > 0
+    assert out[True][0] == out[False][0]
+    assert out[True][2] == out[False][2]
+    for a, b in zip(out[True][1], out[False][1]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
 def test_checkpointing_does_not_change_numerics():
     """Recomputed activations give bit-identical training (deterministic attention)."""
     from torch.nn.attention import SDPBackend, sdpa_kernel
