@@ -37,7 +37,6 @@ allocator, compute-stream pool), host payloads come from its pinned caching
 host allocator.
 """
 
-import heapq
 import os
 import threading
 import time
@@ -103,40 +102,65 @@ class ChunkComm:
 
 
 class _PriorityWorker:
-    """One host thread running host-Adam jobs lowest position first.
+    """One host thread running host-Adam jobs, lowest position first among
+    the jobs whose inputs are ready.
 
     Jobs of CPU-placed positions are submitted in two orders: speculative
     updates during the backward, as each position's gradients become final
     (highest position first: the backward walks the layers in reverse), and
-    the ADAM walk's in-place updates and settles (ascending).  The next
-    forward needs the lowest positions first, so whatever is queued runs in
-    ascending position order; a job already running is not preempted.
-    Futures follow concurrent.futures semantics (``cancel()`` succeeds while
-    the job is still queued)."""
+    the ADAM walk's in-place updates and settles (ascending).  The host
+    enqueues the backward far ahead of the device, so a speculative job is
+    submitted long before its gradients have landed in host memory: each job
+    may carry a ``ready`` predicate (its D2H event has completed), and the
+    worker picks the lowest position among ready jobs — during the backward
+    that is whichever position the device has just finished, at ADAM it is
+    the position the next forward needs first.  A running job is not
+    preempted.  Futures follow concurrent.futures semantics (``cancel()``
+    succeeds while the job is still queued)."""
+
+    POLL_S = 2e-4
 
     def __init__(self):
-        self._heap: List[tuple] = []
+        self._jobs: List[list] = []  # [priority, seq, future, fn, args, ready]
         self._cv = threading.Condition()
         self._seq = 0
+        self._stop = False
         self._thread = threading.Thread(target=self._loop, name="cs-host-adam", daemon=True)
         self._thread.start()
 
-    def submit(self, priority: int, fn, *args) -> Future:
+    def submit(self, priority: int, fn, *args, ready=None) -> Future:
         fut: Future = Future()
         with self._cv:
-            heapq.heappush(self._heap, (priority, self._seq, fut, fn, args))
+            self._jobs.append([priority, self._seq, fut, fn, args, ready])
             self._seq += 1
             self._cv.notify()
         return fut
 
+    def _pick(self):
+        best = None
+        for j in self._jobs:
+            if j[2].cancelled():
+                continue
+            if j[5] is not None and not j[5]():
+                continue
+            if best is None or (j[0], j[1]) < (best[0], best[1]):
+                best = j
+        return best
+
     def _loop(self) -> None:
         while True:
             with self._cv:
-                while not self._heap:
-                    self._cv.wait()
-                _, _, fut, fn, args = heapq.heappop(self._heap)
-            if fn is None:
-                return
+                while True:
+                    if self._stop:
+                        return
+                    self._jobs = [j for j in self._jobs if not j[2].cancelled()]
+                    job = self._pick()
+                    if job is not None:
+                        self._jobs.remove(job)
+                        break
+                    # nothing ready: wait for a submission, or poll readiness
+                    self._cv.wait(self.POLL_S if self._jobs else None)
+            _, _, fut, fn, args, _ = job
             if not fut.set_running_or_notify_cancel():
                 continue
             try:
@@ -146,7 +170,7 @@ class _PriorityWorker:
 
     def shutdown(self) -> None:
         with self._cv:
-            heapq.heappush(self._heap, (float("inf"), self._seq, Future(), None, ()))
+            self._stop = True
             self._cv.notify()
 
 
@@ -598,7 +622,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         if self._worker is None:
             self._worker = _PriorityWorker()
         fut = self._worker.submit(pos, self._run_spec, waits, ins + (n,), shadow + (n,),
-                                  self._spec_state)
+                                  self._spec_state,
+                                  ready=lambda: all(ev.query() for ev in waits))
         self._spec[pos] = (fut, ins, shadow, self._spec_state)
         self.stats.spec_issued += 1
 
@@ -753,6 +778,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         work = self.comm.all_gather_slab(slab, async_op=self.overlap_collectives, src=src)
         if work is not None:
             self._inflight.append((work, (slab,)))
+            if src is not None:
+                # the collective reads the local chunk itself until it completes:
+                # its next writer (the backward's grad overwrite, a K1) and the
+                # slab pool wait for it, exactly as for a gathered remote chunk
+                local_cid = self.chunk_set.param_chunk(pos).chunk_id
+                self._wait_collective(local_cid)
+                self._coll_work[local_cid] = work
         self._coll_end("all_gather", slab, work, t0)
         return slab, work
 

@@ -540,11 +540,16 @@ class ChunkTrainer:
     def step_state(self):
         return self.executor.state.read()
 
-    def local_chunk_payload(self, position: int, kind: ChunkKind = ChunkKind.PARAM_FP16):
-        """The current payload (device preferred) of a local chunk position."""
+    def local_chunk_payload(self, position: int, kind: ChunkKind = ChunkKind.PARAM_FP16,
+                            used_only: bool = True):
+        """The current payload (device preferred) of a local chunk position:
+        its used prefix [0, used_elems) — the tensors packed into it — or,
+        with ``used_only=False``, the full capacity (the tail past the last
+        tensor is unspecified padding)."""
         chunk = self.sim.chunk_set.chunk_at(kind, position)
         ex = self.executor
         for dev in ("gpu", "cpu"):
             if ex.has(chunk, dev):
-                return ex.tensor(chunk, dev)
+                t = ex.tensor(chunk, dev)
+                return t[:chunk.used_elems] if used_only else t
         return None

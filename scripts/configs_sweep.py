@@ -37,8 +37,15 @@ CONFIGS = {
     "12b_mixed": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI, os="auto"),
     "12b_mixed_85": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI, os="auto",
                          gpu_frac=0.85),
+    # the reference's analytic activation curve with the 0.9 HBM budget (the
+    # round-1 default) against the measured warm-up tracer (the default now)
+    "12b_mixed_analytic": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI,
+                               os="auto", nm="analytic"),
+    "12b_ckpt_analytic": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI,
+                              os="auto", ckpt=True, nm="analytic"),
+    "1b_os_cpu": dict(layers=20, hidden=2048, heads=16, batch=32, cap=64 * MI, os="cpu"),
     "1b_b16_emb_plan": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
-                            os="auto"),
+                            os="auto", untied=True),
     "1b_b16_emb_gpu": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
                            os="auto", emb="gpu", untied=True),
 }
@@ -64,7 +71,9 @@ def run_one(name: str) -> dict:
     tr = ChunkTrainer(schema, PolicySpec(capacity_elems=c["cap"], os_placement=c["os"],
                                          checkpointing=c.get("ckpt", False)),
                       hardware=hw, seed=0, hyper=K.AdamHyper(lr=1e-4), cuda_graph=True,
-                      embedding_placement=c.get("emb", "plan"), untied_head=c.get("untied"),
+                      embedding_placement=c.get("emb", "plan"),
+                      untied_head=bool(c.get("untied", False)),
+                      non_model=c.get("nm", "auto"),
                       prefetch_depth=int(os.environ.get("CS_PREFETCH_DEPTH", "2")))
     t_init = time.perf_counter() - t_init
     gen = torch.Generator().manual_seed(3)
@@ -122,6 +131,12 @@ def run_one(name: str) -> dict:
             "prefetch_depth": tr.prefetch_depth, "pinned_alloc_during_timing": pinned,
             "pinned_stats_end": {k: v for k, v in hs1.items() if "current" in k or "peak" in k},
             "embedding_device": tr.embedding_placement,
+            "non_model": "measured" if tr.tracer is not None else "analytic",
+            "gpu_pool_bytes": tr.sim.pools["gpu"].capacity_bytes if hasattr(tr.sim, "pools")
+            else None,
+            "spec_host_adam": [tr.executor.stats.spec_issued, tr.executor.stats.spec_committed,
+                               tr.executor.stats.spec_discarded,
+                               tr.executor.stats.spec_cancelled],
             "host_embedding_s_per_step": (round(tr.host_embedding.host_seconds /
                                                 max(1, tr.iteration), 4)
                                           if tr.host_embedding is not None else 0.0),
