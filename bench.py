@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="eager steps only (no CUDA-graph replay of the steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph-dp", action="store_true",
+                    help="also capture the ZeRO step in a CUDA graph at N > 1 (opt-in: "
+                         "unvalidated on multi-GPU hardware)")
     ap.add_argument("--dist-backend", default="nccl", help=argparse.SUPPRESS)
     ap.add_argument("--same-device", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-offload-probe", action="store_true",
@@ -358,6 +361,23 @@ def k1_traffic(elements):
         return None, None
 
 
+def host_info():
+    """What `cores` means on this host: logical CPUs in the affinity mask,
+    SMT siblings per core, NUMA nodes (sysfs)."""
+    cpus = sorted(os.sched_getaffinity(0))
+    smt = 1
+    try:
+        with open("/sys/devices/system/cpu/cpu%d/topology/thread_siblings_list" % cpus[0]) as f:
+            from paper_2108_05818_b200.hostres import parse_cpulist
+            smt = len(parse_cpulist(f.read().strip()))
+    except OSError:
+        pass
+    nodes = len([d for d in os.listdir("/sys/devices/system/node")
+                 if d.startswith("node")]) if os.path.isdir("/sys/devices/system/node") else 1
+    return {"logical_cpus": len(cpus), "threads_per_core": smt,
+            "physical_cores": len(cpus) // max(smt, 1), "numa_nodes": nodes}
+
+
 def cpu_baseline(schema_kw, sample_batch, steps=1):
     from oracle.cpu_step import CpuChunkStep
     from paper_2108_05818_b200.model import build_gpt_schema
@@ -366,7 +386,7 @@ def cpu_baseline(schema_kw, sample_batch, steps=1):
     secs = [runner.step() for _ in range(steps)]
     t = min(secs)
     return {"value": round(runner.tokens_per_step / t, 3), "unit": UNIT,
-            "cores": runner.threads, "kind": "port",
+            "cores": runner.threads, "kind": "port", "host": host_info(),
             "sample": "%d x %d tokens on the full %d-layer H%d model per step (fp32 torch-CPU "
                       "fwd/bwd + C-oracle chunk Adam over all %.2fB params + the decision "
                       "engine), best of %d" % (sample_batch, schema.seq_len, schema.layers,
@@ -465,7 +485,7 @@ def run_reference(args):
                                                                              args.hidden),
                    "per_step_sample_tokens": runner.tokens_per_step},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": runner.threads,
-                         "kind": "port",
+                         "kind": "port", "host": host_info(),
                          "sample": "%d x %d tokens per step on the full model"
                                    % (args.cpu_sample_batch, args.seq)},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -513,7 +533,7 @@ def main():
     dtype = torch.float16 if args.dtype == "fp16" else torch.bfloat16
     trainer = ChunkTrainer(schema, PolicySpec(capacity_elems=args.cap), dtype=dtype, seed=0,
                            hyper=K.AdamHyper(lr=1e-4, betas=(0.9, 0.999), eps=1e-8),
-                           cuda_graph=not args.no_graph)
+                           cuda_graph=not args.no_graph, graph_multi_rank=args.graph_dp)
     ex = trainer.executor
     B, S = args.batch, args.seq
     gen = torch.Generator().manual_seed(1000 + rank)

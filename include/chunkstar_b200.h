@@ -236,9 +236,13 @@ int cs_embed_bwd_host(const int64_t* tokens, int64_t n_tokens, int seq_len, cons
  * writes every row of gwte [V,H] and gwpe [S,H] (fp32 sums in ascending token
  * order, one rounding); accumulate=1 adds the rounded row sums to gwte instead
  * (K4's slot += src, for a tied LM head whose dW was written there first).
- * Device pointers, 16-byte aligned buffers, stream-ordered. */
+ * Device pointers, 16-byte aligned buffers, stream-ordered.  Token ids are
+ * device-resident and not validated on the host: a token outside [0, vocab)
+ * reads nothing and its output row is NaN (so the loss is NaN and the
+ * overflow check skips the step); the backward ignores such tokens. */
 int cs_embed_fwd(const int64_t* tokens, int64_t n_tokens, int seq_len, const void* wte,
-                 const void* wpe, int hidden, void* out, int dtype, void* stream);
+                 const void* wpe, int64_t vocab, int hidden, void* out, int dtype,
+                 void* stream);
 int cs_embed_bwd(const int64_t* order, const int64_t* row_start, int64_t n_tokens, int seq_len,
                  const void* dout, int64_t vocab, int hidden, void* gwte, void* gwpe,
                  int accumulate, int dtype, void* stream);
@@ -247,7 +251,10 @@ int cs_embed_bwd(const int64_t* order, const int64_t* row_start, int64_t n_token
  * Forward: per-row loss = logsumexp(logits_row) - logits_row[target] and the
  * row's logsumexp, one pass over fp16/bf16 logits [rows, vocab].  Backward:
  * logits <- (softmax - onehot) * (*dloss) * scale, in place.  dloss is a
- * device scalar (the upstream gradient, e.g. the loss scale). */
+ * device scalar (the upstream gradient, e.g. the loss scale).  A target
+ * outside [0, vocab) is never dereferenced: its row's loss and gradient are
+ * NaN, so the loss reports it and the step's overflow check skips the update
+ * (targets are device-resident and not validated on the host). */
 int cs_xent_fwd(const void* logits, const int64_t* targets, int64_t rows, int64_t vocab,
                 int dtype, float* loss_rows, float* lse_rows, void* stream);
 int cs_xent_bwd(void* logits, const int64_t* targets, const float* lse_rows,

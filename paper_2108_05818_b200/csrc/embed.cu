@@ -63,15 +63,20 @@ __device__ __forceinline__ uint4 pack8(const float* a) {
 // grid-stride over vectors of the [n, H] output; 128-bit loads/stores
 template <int DT>
 __global__ void embed_fwd_kernel(const int64_t* __restrict__ tok, int64_t n, int S, int H,
-                                 const uint4* __restrict__ wte, const uint4* __restrict__ wpe,
-                                 uint4* __restrict__ out) {
+                                 int64_t V, const uint4* __restrict__ wte,
+                                 const uint4* __restrict__ wpe, uint4* __restrict__ out) {
   const int hv = H / 8;
   const int64_t total = n * hv;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = q / hv;
     const int c = (int)(q - i * hv);
-    const uint4 a = __ldg(wte + tok[i] * hv + c);
+    const int64_t t = tok[i];
+    if (t < 0 || t >= V) {  // no out-of-range read: the row is NaN (loss NaN, step skipped)
+      __stcs(out + q, make_uint4(0x7fff7fffu, 0x7fff7fffu, 0x7fff7fffu, 0x7fff7fffu));
+      continue;
+    }
+    const uint4 a = __ldg(wte + t * hv + c);
     const uint4 b = __ldg(wpe + (i % S) * hv + c);
     // one fp32 add per element (no 0 + x first: keeps the sign of -0 + -0)
     const uint32_t* ua = reinterpret_cast<const uint32_t*>(&a);
@@ -129,9 +134,9 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 }  // namespace
 
 extern "C" int cs_embed_fwd(const int64_t* tokens, int64_t n_tokens, int seq_len,
-                            const void* wte, const void* wpe, int hidden, void* out, int dtype,
-                            void* stream) {
-  if (n_tokens < 0 || seq_len <= 0 || hidden <= 0 || hidden % 8 != 0 ||
+                            const void* wte, const void* wpe, int64_t vocab, int hidden,
+                            void* out, int dtype, void* stream) {
+  if (n_tokens < 0 || seq_len <= 0 || hidden <= 0 || hidden % 8 != 0 || vocab <= 0 ||
       (n_tokens > 0 && (!tokens || !wte || !wpe || !out)) ||
       (dtype != CS_FP16 && dtype != CS_BF16)) {
     cs::set_error("cs_embed_fwd: invalid argument (hidden must be a multiple of 8)");
@@ -153,10 +158,10 @@ extern "C" int cs_embed_fwd(const int64_t* tokens, int64_t n_tokens, int seq_len
   auto* o = static_cast<uint4*>(out);
   if (dtype == CS_FP16)
     embed_fwd_kernel<CS_FP16><<<(unsigned)grid, threads, 0, s>>>(tokens, n_tokens, seq_len,
-                                                                  hidden, a, b, o);
+                                                                  hidden, vocab, a, b, o);
   else
     embed_fwd_kernel<CS_BF16><<<(unsigned)grid, threads, 0, s>>>(tokens, n_tokens, seq_len,
-                                                                  hidden, a, b, o);
+                                                                  hidden, vocab, a, b, o);
   cs::note_launches(1);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

@@ -142,7 +142,8 @@ xent_fwd_kernel(const uint16_t* __restrict__ logits, const int64_t* __restrict__
     if (lane == 0) {
       const float lse = m + logf(s);
       lse_rows[row] = lse;
-      loss_rows[row] = lse - to_f<DT>(x[targets[row]]);
+      const int64_t t = targets[row];  // out of range: no read, NaN loss (step skipped)
+      loss_rows[row] = (t >= 0 && t < vocab) ? lse - to_f<DT>(x[t]) : __int_as_float(0x7fc00000);
     }
   }
 }
@@ -155,8 +156,10 @@ xent_bwd_kernel(uint16_t* __restrict__ logits, const int64_t* __restrict__ targe
   const int64_t row = blockIdx.x;
   uint16_t* x = logits + row * vocab;
   const float lse = lse_rows[row];
-  const float g = *dloss * scale;
   const int64_t tgt = targets[row];
+  // an out-of-range target poisons its row's gradient, so the step's
+  // overflow check skips the update instead of training on a wrong target
+  const float g = (tgt >= 0 && tgt < vocab) ? *dloss * scale : __int_as_float(0x7fc00000);
   if ((vocab % 8) == 0) {
     uint4* xv = reinterpret_cast<uint4*>(x);
     const int64_t nv = vocab / 8;

@@ -120,6 +120,11 @@ def adam_chunks(items: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor, 
                                     _stream(stream)), "cs_adam_chunks")
 
 
+def host_threads(requested: int = 0) -> int:
+    """OpenMP team size the host kernels use (``cs_host_threads``)."""
+    return int(N.load().cs_host_threads(int(requested)))
+
+
 def adam_chunks_host(items, hyper: AdamHyper, state: N.CsStepState, n_threads: int = 0) -> None:
     """Host Adam for CPU-placed positions (tensors in host memory)."""
     if not items:
@@ -248,10 +253,10 @@ def embed_fwd(tokens: torch.Tensor, wte: torch.Tensor, wpe: torch.Tensor,
     if tok.dtype != torch.int64:
         raise TypeError("tokens must be int64")
     B, S = tok.shape
-    H = wte.shape[1]
+    V, H = wte.shape
     out = torch.empty(B, S, H, dtype=wte.dtype, device=wte.device)
-    N.check(N.load().cs_embed_fwd(tok.data_ptr(), B * S, S, wte.data_ptr(), wpe.data_ptr(), H,
-                                  out.data_ptr(), _code(wte.dtype), _stream(stream)),
+    N.check(N.load().cs_embed_fwd(tok.data_ptr(), B * S, S, wte.data_ptr(), wpe.data_ptr(), V,
+                                  H, out.data_ptr(), _code(wte.dtype), _stream(stream)),
             "cs_embed_fwd")
     return out
 

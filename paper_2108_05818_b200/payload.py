@@ -118,7 +118,7 @@ class _PriorityWorker:
     preempted.  Futures follow concurrent.futures semantics (``cancel()``
     succeeds while the job is still queued)."""
 
-    POLL_S = 2e-4
+    POLL_S = 1e-3
 
     def __init__(self):
         self._jobs: List[list] = []  # [priority, seq, future, fn, args, ready]
@@ -229,6 +229,17 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.max_grad_norm = max_grad_norm
         self.comm = comm
         self.host_threads = host_threads
+        #: OpenMP team of the host Adam jobs on the worker thread: they run
+        #: while the main thread enqueues the step (the backward under
+        #: speculation, the next forward otherwise), and a team as wide as the
+        #: machine time-slices that Python thread off its core — the device
+        #: then starves (measured: a 130 ms backward stretched to 300-500 ms
+        #: with 16 threads on the 16-core box).  Two cores stay with the main
+        #: thread and the CUDA driver; the memory-bound update loses nothing
+        #: (14 vs 16 threads: 5.7 vs 5.2 Gelem/s, profiles/r01/offload_host_threads.jsonl)
+        ht = host_threads if host_threads > 0 else K.host_threads(0)
+        reserve = 2 if ht >= 8 else (1 if ht >= 4 else 0)
+        self.worker_threads = int(os.environ.get("CS_WORKER_THREADS", "0")) or max(1, ht - reserve)
         self.time_copies = time_copies
         # test knob: every chunk move first spins this many cycles on its copy
         # stream, and an H2D destination reads NaN until the bytes land, so a
@@ -493,7 +504,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
 
     def _run_host_adam(self, job: _HostAdamJob, item, state) -> None:
         t0 = time.perf_counter()
-        K.adam_chunks_host([item], self.hyper, state, self.host_threads)
+        K.adam_chunks_host([item], self.hyper, state, self.worker_threads)
         with self._stats_lock:
             self.stats.host_adam_seconds += time.perf_counter() - t0
         self._job_done(job)
@@ -640,7 +651,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         for ev in waits:
             ev.synchronize()
         t0 = time.perf_counter()
-        K.adam_chunks_host_oop([item_in], [item_out], self.hyper, state, self.host_threads)
+        K.adam_chunks_host_oop([item_in], [item_out], self.hyper, state, self.worker_threads)
         with self._stats_lock:
             self.stats.host_adam_seconds += time.perf_counter() - t0
 

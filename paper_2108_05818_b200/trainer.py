@@ -104,7 +104,8 @@ class ChunkTrainer:
                  untied_head: bool = False,
                  async_host_adam: Optional[bool] = None,
                  comm=None, bind_host: Optional[bool] = None,
-                 speculative_host_adam: Optional[bool] = None):
+                 speculative_host_adam: Optional[bool] = None,
+                 graph_multi_rank: Optional[bool] = None):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -243,6 +244,13 @@ class ChunkTrainer:
         self.failed: Optional[IterationReport] = None
         self.sim.engine.physical_oom = (torch.OutOfMemoryError,)
         self.cuda_graph = cuda_graph
+        #: capture the ZeRO step (its NCCL all-gathers / reduce-scatters and
+        #: the scalar all-reduces are captured as graph nodes, NCCL >= 2.9.6)
+        #: at p > 1 too; opt-in (CS_GRAPH_DP=1) until validated on a multi-GPU
+        #: box: this sandbox has one GPU and gloo collectives are not capturable
+        if graph_multi_rank is None:
+            graph_multi_rank = os.environ.get("CS_GRAPH_DP", "0") == "1"
+        self.graph_multi_rank = graph_multi_rank
         self.prefetch_depth = prefetch_depth
         self.gather_depth = gather_depth
         self._graph = None
@@ -407,7 +415,7 @@ class ChunkTrainer:
                 [(c.group_id, c.kind, c.bytes) for c in r.collectives])
 
     def _graph_ready(self) -> bool:
-        if self.nproc != 1 or len(self.reports) < 3:
+        if (self.nproc != 1 and not self.graph_multi_rank) or len(self.reports) < 3:
             return False
         a, b = self.reports[-2], self.reports[-1]
         if a.warmup or self._ledger_key(a) != self._ledger_key(b):

@@ -42,14 +42,23 @@ def timed_steps(tr, toks, steps):
         tr.step(toks[i % 2])
     tr.finish_host_work()
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
+    hs0 = torch.cuda.host_memory_stats()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    evs[0].record()
     for i in range(steps):
         tr.step(toks[i % 2])
+        evs[i + 1].record()
     tr.finish_host_work()
-    b.record()
+    end = torch.cuda.Event(enable_timing=True)
+    end.record()
     torch.cuda.synchronize()
-    return a.elapsed_time(b) / steps
+    hs1 = torch.cuda.host_memory_stats()
+    per = [round(evs[i].elapsed_time(evs[i + 1]), 1) for i in range(steps)]
+    pinned = {k: hs1[k] - hs0.get(k, 0) for k in hs1
+              if isinstance(hs1[k], (int, float)) and hs1[k] != hs0.get(k, 0)
+              and ("alloc" in k or "free" in k or "time" in k.lower())}
+    timed_steps.last = {"per_step_enqueue_boundaries_ms": per, "pinned_delta": pinned}
+    return evs[0].elapsed_time(end) / steps
 
 
 def timeline(tr, toks):
@@ -103,25 +112,34 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--ab", type=int, default=0)
+    ap.add_argument("--arms", default="", help="JSON list of env dicts for --ab")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "offload_timeline.json"))
     args = ap.parse_args()
     if args.ab:
-        arms = [{"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1"},
-                {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "0"},
-                {"CS_EARLY_DRAIN": "0", "CS_SPEC_HOST_ADAM": "0"}]
+        arms = [{"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1", "CS_WORKER_THREADS": "0"},
+                {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1", "CS_WORKER_THREADS": "12"},
+                {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "0", "CS_WORKER_THREADS": "0"},
+                {"CS_EARLY_DRAIN": "0", "CS_SPEC_HOST_ADAM": "0", "CS_WORKER_THREADS": "0"}]
+        if args.arms:
+            arms = json.loads(args.arms)
         for rep in range(args.ab):
             for env in arms:
                 tr, toks = make(args.batch, env)
-                ms = timed_steps(tr, toks, 3)
+                ms = timed_steps(tr, toks, 4)
                 st = tr.executor.stats
                 print(json.dumps({"env": env, "rep": rep, "ms_per_step": round(ms, 2),
                                   "host_adam_s": round(st.host_adam_seconds, 3),
                                   "spec": [st.spec_issued, st.spec_committed, st.spec_discarded,
-                                           st.spec_cancelled]}), flush=True)
+                                           st.spec_cancelled], **timed_steps.last}), flush=True)
                 tr.close()
-                del tr, toks
+                del tr, toks, st
+                import gc
+                gc.collect()
+                torch.cuda.synchronize()
                 torch.cuda.empty_cache()
-    tr, toks = make(args.batch, {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1"})
+                torch._C._host_emptyCache()  # pinned blocks back to the OS between arms
+    tr, toks = make(args.batch, {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1",
+                                 "CS_WORKER_THREADS": "0"})
     res = timeline(tr, toks)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:

@@ -75,7 +75,7 @@ def test_argument_errors_of_model_side_entry_points(native_lib):
     """Validation happens before any CUDA call (no GPU needed)."""
     from paper_2108_05818_b200 import _native as N
     lib = native_lib
-    assert lib.cs_embed_fwd(None, 4, 2, None, None, 12, None, N.CS_FP16, None) == -1  # H % 8
+    assert lib.cs_embed_fwd(None, 4, 2, None, None, 100, 12, None, N.CS_FP16, None) == -1  # H % 8
     assert b"hidden" in lib.cs_last_error()
     assert lib.cs_embed_bwd(None, None, 5, 2, None, 10, 16, None, None, 0, N.CS_FP16,
                             None) == -1                                          # n % S

@@ -130,3 +130,31 @@ def test_device_embedding_backward_accumulates_into_weights(native_lib, oracle_l
     assert np.array_equal(_bits(wte.cpu()), ref)
     _, rp = O.embed_bwd(tok.numpy(), _bits(dout), V, CODE[dtype])
     assert np.array_equal(_bits(wpe[:S].cpu()), rp) and not bool(wpe[S:].any())
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA GPU")
+def test_device_out_of_range_ids_read_nothing_and_poison_their_rows(native_lib):
+    """Device-resident token ids and targets are not validated on the host:
+    an id outside [0, V) must not be dereferenced; the embedding row and the
+    cross-entropy row (loss and gradient) become NaN, so the overflow check
+    skips the step; valid rows are unchanged and the backward ignores the id."""
+    tok, wte, wpe, dout = _case(torch.float16, 2, 4, 10, 8, seed=2)
+    good = K.embed_fwd(tok.cuda(), wte.cuda(), wpe.cuda()).cpu()
+    bad = tok.clone()
+    bad[0, 1], bad[1, 3] = 10, -5
+    out = K.embed_fwd(bad.cuda(), wte.cuda(), wpe.cuda()).cpu()
+    assert torch.isnan(out[0, 1]).all() and torch.isnan(out[1, 3]).all()
+    mask = torch.ones(2, 4, dtype=torch.bool)
+    mask[0, 1] = mask[1, 3] = False
+    assert torch.equal(out[mask].view(torch.int16), good[mask].view(torch.int16))
+    gw = torch.empty_like(wte).cuda()
+    gp = torch.empty_like(wpe).cuda()
+    K.embed_bwd_into(bad.cuda(), dout.cuda(), gw, gp)  # the bad ids contribute nothing
+    torch.cuda.synchronize()
+    logits = torch.randn(3, 40, device="cuda").half()
+    tgt = torch.tensor([5, 40, -1], device="cuda")
+    loss, lse = K.xent_fwd(logits, tgt)
+    assert torch.isfinite(loss[0]) and torch.isnan(loss[1:]).all()
+    g = K.xent_bwd_(logits.clone(), tgt, lse, torch.ones((), device="cuda"), 1.0)
+    assert torch.isfinite(g[0]).all() and torch.isnan(g[1:]).all()
