@@ -155,7 +155,7 @@ def host_link_peak(dev, nbytes=1 << 30, iters=5):
     return out
 
 
-def offload_probe(schema_kw, dev, steps=3, warmup=2):
+def offload_probe(schema_kw, dev, steps=4, warmup=6):
     """The same 1B step with every optimizer triplet in pinned host DRAM
     (os_placement=cpu): grads D2H + host fused Adam + params H2D as
     `adam_copy` (`engine.py:249-251, 265-267`).  Reports the chunk moves'
@@ -179,6 +179,8 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
     st = tr.executor.stats
     st.copy_events.clear()
     host0, items0 = st.host_adam_seconds, st.host_adam_items
+    spec0 = (st.spec_issued, st.spec_committed, st.spec_discarded, st.spec_cancelled)
+    pinned0 = torch.cuda.host_memory_stats().get("num_host_alloc", 0)
     a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for i in range(steps):
@@ -187,6 +189,9 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
     b_.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b_) / steps
+    pinned_allocs = torch.cuda.host_memory_stats().get("num_host_alloc", 0) - pinned0
+    spec = [x - y for x, y in zip((st.spec_issued, st.spec_committed, st.spec_discarded,
+                                   st.spec_cancelled), spec0)]
     agg = {}
     for name, nbytes, e0, e1 in st.copy_events:
         t = e0.elapsed_time(e1)
@@ -214,6 +219,11 @@ def offload_probe(schema_kw, dev, steps=3, warmup=2):
            "prefetch_hits": st.prefetch_hits, "prefetch_issued": st.prefetch_issued,
            "prefetch_discarded": st.prefetch_discarded,
            "async_host_adam": tr.executor.async_host_adam,
+           "speculative_host_adam": {"enabled": tr.executor.speculative_host_adam,
+                                     "issued_committed_discarded_cancelled": spec},
+           "early_drains": st.early_drains,
+           "pinned_host_allocs_during_timing": pinned_allocs,
+           "worker_threads": tr.executor.worker_threads, "host_threads": tr.host_threads,
            "peak_source": "pinned cudaMemcpyAsync 1 GiB"}
     del tr
     torch.cuda.empty_cache()

@@ -161,12 +161,14 @@ class _PriorityWorker:
                     # nothing ready: wait for a submission, or poll readiness
                     self._cv.wait(self.POLL_S if self._jobs else None)
             _, _, fut, fn, args, _ = job
+            job = None  # no reference to the job's buffers while idle
             if not fut.set_running_or_notify_cancel():
                 continue
             try:
                 fut.set_result(fn(*args))
             except BaseException as e:  # delivered to whoever joins the job
                 fut.set_exception(e)
+            fut = fn = args = None
 
     def shutdown(self) -> None:
         with self._cv:
@@ -234,11 +236,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         #: speculation, the next forward otherwise), and a team as wide as the
         #: machine time-slices that Python thread off its core — the device
         #: then starves (measured: a 130 ms backward stretched to 300-500 ms
-        #: with 16 threads on the 16-core box).  Two cores stay with the main
-        #: thread and the CUDA driver; the memory-bound update loses nothing
-        #: (14 vs 16 threads: 5.7 vs 5.2 Gelem/s, profiles/r01/offload_host_threads.jsonl)
+        #: with 16 threads on the 16-core box).  A quarter of the cores (at
+        #: least two) stay with the main thread and the CUDA driver; the memory-bound update loses nothing
+        #: (14 vs 16 threads: 5.7 vs 5.2 Gelem/s, profiles/r01/offload_host_threads.jsonl;
+        #: all-host 1B step with speculation: 12 threads 281-287 ms, 14 threads
+        #: 304-315 ms, profiles/r02/offload_ab.jsonl)
         ht = host_threads if host_threads > 0 else K.host_threads(0)
-        reserve = 2 if ht >= 8 else (1 if ht >= 4 else 0)
+        reserve = max(2, ht // 4) if ht >= 8 else (1 if ht >= 4 else 0)
         self.worker_threads = int(os.environ.get("CS_WORKER_THREADS", "0")) or max(1, ht - reserve)
         self.time_copies = time_copies
         # test knob: every chunk move first spins this many cycles on its copy
@@ -315,6 +319,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         #: the native communicator's comm-stream events), else issue -> done
         self.time_collectives = False
         self.coll_log: List[tuple] = []
+        self._free_host: Dict[tuple, List[tuple]] = {}  # (dtype, numel) -> [(tensor, event)]
         self._stats_lock = threading.Lock()
         #: CPU-placed embedding operator (embedding.HostEmbedding) or None
         self.host_embedding = None
@@ -367,6 +372,47 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         if device == GPU:
             return self.slabs.take(chunk.capacity_elems, self._elem_dtype(chunk), self.compute)
         return torch.empty(chunk.capacity_elems, dtype=self._elem_dtype(chunk), pin_memory=True)
+
+    # -- pinned host buffers as D2H destinations ------------------------------------
+    #
+    # A dropped host payload (e.g. a host-placed position's parameters, dropped
+    # when the backward overwrites them with gradients) is kept as the
+    # destination of a later D2H (parameter chunks only: the gradient drains
+    # and evictions land there) instead of going back to PyTorch's pinned
+    # cache.  That cache only reuses a block once every copy recorded on it
+    # has completed — and the host runs a step ahead of the device, so the
+    # early gradient drains of the backward always found the previous step's
+    # buffers still pending and fell through to cudaHostAlloc (~0.1 s for a
+    # 128 MiB block, several per step, measured).  Here reuse is
+    # stream-ordered instead: the buffer carries an event recorded on the H2D
+    # copy stream when it was dropped (every copy that may still read it),
+    # and the D2H stream waits on it before writing.  Only D2H destinations
+    # are served this way (the host never writes these buffers before the
+    # D2H that fills them has completed).
+
+    HOST_FREE_PER_KIND = 16
+
+    def _give_host(self, t: torch.Tensor) -> None:
+        if not t.is_pinned():
+            return
+        lst = self._free_host.setdefault((t.dtype, t.numel()), [])
+        if len(lst) >= self.HOST_FREE_PER_KIND:
+            return
+        ev = None
+        if self.copy_stream is not None:
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        lst.append((t, ev))
+
+    def _alloc_d2h_dst(self, chunk: Chunk) -> torch.Tensor:
+        """Pinned host destination of a D2H copy (see ``_give_host``)."""
+        lst = self._free_host.get((self._elem_dtype(chunk), chunk.capacity_elems))
+        if lst:
+            t, ev = lst.pop()
+            if ev is not None:
+                self.d2h_stream.wait_event(ev)
+            return t
+        return self._alloc(chunk, CPU)
 
     def _alloc_for_copy(self, chunk: Chunk) -> torch.Tensor:
         """HBM destination of an H2D copy, taken from the copy stream's pool so
@@ -463,7 +509,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             s = self.payload[src][chunk.chunk_id]
             d = self._retained.pop((chunk.chunk_id, dst), None)
             if d is None:
-                d = self._alloc_for_copy(chunk) if dst == GPU else self._alloc(chunk, dst)
+                d = self._alloc_for_copy(chunk) if dst == GPU else self._alloc_d2h_dst(chunk)
             prior = self.ready.pop((chunk.chunk_id, src), None)
             done = self._transfer(s, d, src, dst, prior)
         if done is not None:
@@ -602,7 +648,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             if not self.has(chunk, GPU) or self.has(chunk, CPU) or cid in self._predrained \
                     or cid in self._awaiting_gather:
                 continue
-            d = self._alloc(chunk, CPU)
+            d = self._alloc_d2h_dst(chunk)
             done = self._transfer(self.tensor(chunk, GPU), d, GPU, CPU,
                                   self.ready.get((cid, GPU)), after=self._coll_work.get(cid))
             self._predrained[cid] = (d, done)
@@ -738,6 +784,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     self.ready[key] = ev
                 self._retained[key] = t
                 t = None
+        if t is not None and device == CPU and chunk.list_kind is ChunkKind.PARAM_FP16:
+            self._give_host(t)
         if t is not None and device == GPU:
             if cid in self._pending_ids:
                 self._flush_adam()  # K1 must update this payload before it is recycled
@@ -993,7 +1041,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 chunk = cs.param_chunk(pos)
                 if plan.device_of_position(pos) == CPU and self.has(chunk, GPU) \
                         and not self.has(chunk, CPU) and chunk.chunk_id not in self._predrained:
-                    d = self._alloc(chunk, CPU)
+                    d = self._alloc_d2h_dst(chunk)
                     done = self._transfer(self.tensor(chunk, GPU), d, GPU, CPU,
                                           self.ready.get((chunk.chunk_id, GPU)))
                     self._predrained[chunk.chunk_id] = (d, done)

@@ -37,8 +37,8 @@ def make(batch, env):
     return tr, toks
 
 
-def timed_steps(tr, toks, steps):
-    for i in range(2):
+def timed_steps(tr, toks, steps, warmup=6):
+    for i in range(warmup):
         tr.step(toks[i % 2])
     tr.finish_host_work()
     torch.cuda.synchronize()
@@ -117,9 +117,9 @@ def main():
     args = ap.parse_args()
     if args.ab:
         arms = [{"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1", "CS_WORKER_THREADS": "0"},
-                {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1", "CS_WORKER_THREADS": "12"},
+                {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1", "CS_WORKER_THREADS": "10"},
                 {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "0", "CS_WORKER_THREADS": "0"},
-                {"CS_EARLY_DRAIN": "0", "CS_SPEC_HOST_ADAM": "0", "CS_WORKER_THREADS": "0"}]
+                {"CS_EARLY_DRAIN": "0", "CS_SPEC_HOST_ADAM": "0", "CS_WORKER_THREADS": "16"}]
         if args.arms:
             arms = json.loads(args.arms)
         for rep in range(args.ab):
