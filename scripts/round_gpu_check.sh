@@ -1,0 +1,25 @@
+#!/bin/bash
+# Full GPU evidence pass for one round (run under gpurun from the repo root):
+# GPU test suite, the default bench line, the ncu launch list of one
+# post-warm-up step, an ncu --set full capture of the in-step K1 launch, the
+# C5 microbench with CPU arms, and the single-GPU configuration sweep.
+# Everything lands in gpurun_out/<tag>_*.
+tag=${1:-r02}
+out=gpurun_out
+mkdir -p $out
+python -c "import __graft_entry__ as g; g.build()" > $out/${tag}_build.log 2>&1
+python -m pytest tests -m gpu -x -q > $out/${tag}_gputest.log 2>&1; echo rc=$? >> $out/${tag}_gputest.log
+python bench.py > $out/${tag}_bench.log 2>&1; echo rc=$? >> $out/${tag}_bench.log
+ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+    --log-file $out/${tag}_step_launches.csv \
+    python bench.py --profile-step --warmup 3 --no-cpu-baseline --no-offload-probe --no-c5 \
+    > $out/${tag}_ncu_launches.log 2>&1
+ncu --set full --clock-control none --import-source on --profile-from-start off \
+    -k regex:adam_tma -c 1 -f -o $out/${tag}_k1_insitu \
+    python bench.py --profile-step --warmup 3 --no-cpu-baseline --no-offload-probe --no-c5 \
+    > $out/${tag}_ncu_k1.log 2>&1
+ncu -i $out/${tag}_k1_insitu.ncu-rep --page raw --csv > $out/${tag}_k1_insitu_raw.csv 2>/dev/null
+python -m paper_2108_05818_b200.microbench --cpu > $out/${tag}_microbench_c5.jsonl 2>&1
+python scripts/configs_sweep.py ${SWEEP:-12b_mixed 12b_ckpt 12b_mixed_analytic 1b_os_cpu 4b_gpu} \
+    > $out/${tag}_configs_sweep.jsonl 2>&1
+echo done
