@@ -26,12 +26,15 @@ from paper_2108_05818_b200.model import build_gpt_schema  # noqa: E402
 from paper_2108_05818_b200.trainer import ChunkTrainer  # noqa: E402
 
 
-def make(batch, env):
+MODELS = {"1b": dict(layers=20, hidden_dim=2048, heads=16),
+          "12b": dict(layers=60, hidden_dim=4096, heads=32)}
+
+
+def make(batch, env, model="1b", os_placement="cpu"):
     os.environ.update(env)
-    schema = build_gpt_schema(layers=20, hidden_dim=2048, heads=16, seq_len=1024, vocab=50304,
-                              batch=batch)
-    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=64 << 20, os_placement="cpu"), seed=0,
-                      hyper=K.AdamHyper(lr=1e-4), time_copies=True)
+    schema = build_gpt_schema(**MODELS[model], seq_len=1024, vocab=50304, batch=batch)
+    tr = ChunkTrainer(schema, PolicySpec(capacity_elems=64 << 20, os_placement=os_placement),
+                      seed=0, hyper=K.AdamHyper(lr=1e-4), time_copies=True)
     gen = torch.Generator().manual_seed(7)
     toks = [torch.randint(0, schema.vocab, (batch, 1025), generator=gen).cuda() for _ in range(2)]
     return tr, toks
@@ -108,9 +111,51 @@ def timeline(tr, toks):
     return {"events": ev, "copies": copies, "host_adam": host}
 
 
+def _busy(windows):
+    """Union length of [a, b) windows (ms)."""
+    tot, end = 0.0, None
+    for a, b in sorted(windows):
+        if end is None or a > end:
+            tot += b - a
+            end = b
+        elif b > end:
+            tot += b - end
+            end = b
+    return round(tot, 1)
+
+
+def summarize(res):
+    """Per phase of the FIRST recorded step (GPU clock): window, bytes and
+    busy time of each copy direction inside it, host-Adam busy time."""
+    ev = res["events"]
+    starts = {}
+    for i, n, k, h, g in ev:
+        starts.setdefault((i, k), []).append(g)
+    first = lambda key: starts[key][0]
+    idx = sorted({i for i, *_ in ev})
+    adam = idx[-1]
+    n_fwd = (len(idx) - 1) // 2
+    bounds = {"fwd": (first((idx[0], "start")), first((idx[n_fwd], "start"))),
+              "bwd": (first((idx[n_fwd], "start")), first((adam, "start"))),
+              "adam": (first((adam, "start")), starts[(idx[0], "start")][1])}
+    out = {"step_ms": round(bounds["adam"][1] - bounds["fwd"][0], 1)}
+    for ph, (a, b) in bounds.items():
+        d = {"window_ms": round(b - a, 1)}
+        for kind in ("gpu>cpu", "cpu>gpu"):
+            w = [(max(x, a), min(y, b)) for n, x, y, nb in res["copies"] if n == kind and y > a and x < b]
+            nb = sum(nb for n, x, y, nb in res["copies"] if n == kind and a <= x < b)
+            d[kind] = {"busy_ms": _busy(w), "gb_started": round(nb / 1e9, 2)}
+        d["host_adam_busy_ms"] = _busy([(max(x, a), min(y, b)) for c, x, y in res["host_adam"]
+                                        if y > a and x < b])
+        out[ph] = d
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--model", default="1b", choices=sorted(MODELS))
+    ap.add_argument("--os", default="cpu", help="os_placement (auto|cpu|gpu)")
     ap.add_argument("--ab", type=int, default=0)
     ap.add_argument("--arms", default="", help="JSON list of env dicts for --ab")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "offload_timeline.json"))
@@ -124,7 +169,7 @@ def main():
             arms = json.loads(args.arms)
         for rep in range(args.ab):
             for env in arms:
-                tr, toks = make(args.batch, env)
+                tr, toks = make(args.batch, env, args.model, args.os)
                 ms = timed_steps(tr, toks, 4)
                 st = tr.executor.stats
                 print(json.dumps({"env": env, "rep": rep, "ms_per_step": round(ms, 2),
@@ -139,8 +184,15 @@ def main():
                 torch.cuda.empty_cache()
                 torch._C._host_emptyCache()  # pinned blocks back to the OS between arms
     tr, toks = make(args.batch, {"CS_EARLY_DRAIN": "1", "CS_SPEC_HOST_ADAM": "1",
-                                 "CS_WORKER_THREADS": "0"})
+                                 "CS_WORKER_THREADS": "0"}, args.model, args.os)
     res = timeline(tr, toks)
+    res["summary"] = summarize(res)
+    st = tr.executor.stats
+    res["summary"]["exec_stats"] = {k: getattr(st, k) for k in (
+        "prefetch_issued", "prefetch_hits", "prefetch_discarded", "adam_prefetch_early",
+        "adam_prefetch_oom", "preevict_issued", "preevict_hits", "preevict_discarded",
+        "early_drains", "spec_issued", "spec_committed", "spec_cancelled")}
+    print(json.dumps(res["summary"]))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(res, f)
