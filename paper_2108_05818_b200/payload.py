@@ -211,6 +211,12 @@ class ExecStats:
     spec_committed: int = 0
     spec_discarded: int = 0
     spec_cancelled: int = 0
+    adam_prefetch_early: int = 0
+    adam_prefetch_oom: int = 0
+    preevict_issued: int = 0
+    preevict_hits: int = 0
+    preevict_discarded: int = 0
+    preevict_discarded_bytes: int = 0
     copy_events: List[Tuple[str, int, "torch.cuda.Event", "torch.cuda.Event"]] = field(
         default_factory=list)
 
@@ -273,6 +279,24 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._predrained: Dict[int, Tuple[torch.Tensor, "torch.cuda.Event"]] = {}
         self._prefetch_sched: Dict[int, List[int]] = {}
         self.prefetch_depth = 0
+        #: ADAM-time fetches issued during the backward, as early as the last
+        #: iteration's per-moment GPU usage leaves room for them (event -> ids)
+        self._adam_prefetch_at: Dict[int, List[int]] = {}
+        #: bytes of HBM left unplanned when placing those early fetches
+        self.adam_prefetch_margin = float(os.environ.get("CS_ADAM_PREFETCH_MARGIN", "0.03"))
+        self.early_adam_prefetch = os.environ.get("CS_EARLY_ADAM_PREFETCH", "1") != "0"
+        #: pre-eviction: an optimizer-state chunk the last iteration evicted
+        #: during FWD/BWD is only ever written by K1, so its D2H can start
+        #: right after this ADAM's K1 -- when the D2H direction is idle (ADAM
+        #: fetches saturate H2D) -- instead of at the eviction moment in the
+        #: next forward, where the activations are waiting for its HBM.  The
+        #: accounting's eviction then adopts the landed host copy
+        self.preevict = os.environ.get("CS_PREEVICT", "1") != "0"
+        self._preevict_ids: Set[int] = set()
+        self._preevicted: Dict[int, Tuple[torch.Tensor, "torch.cuda.Event"]] = {}
+        #: with pre-evictions pending, K1 launches every this many positions
+        #: so their D2Hs start during the ADAM walk
+        self.preevict_batch = 4
         self._plan = None
         self._host_state = None
         self._state_snap = None
@@ -390,16 +414,17 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     # are served this way (the host never writes these buffers before the
     # D2H that fills them has completed).
 
-    HOST_FREE_PER_KIND = 16
+    HOST_FREE_PER_KIND = 256
 
-    def _give_host(self, t: torch.Tensor) -> None:
+    def _give_host(self, t: torch.Tensor, ev: Optional["torch.cuda.Event"] = None) -> None:
+        """``ev``: the last device work on ``t`` (default: whatever the H2D
+        stream has enqueued so far, i.e. every copy that may still read it)."""
         if not t.is_pinned():
             return
         lst = self._free_host.setdefault((t.dtype, t.numel()), [])
         if len(lst) >= self.HOST_FREE_PER_KIND:
             return
-        ev = None
-        if self.copy_stream is not None:
+        if ev is None and self.copy_stream is not None:
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         lst.append((t, ev))
@@ -500,6 +525,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             hit = self._prefetched.pop(chunk.chunk_id, None)
         else:
             hit = self._predrained.pop(chunk.chunk_id, None)
+            if hit is None:
+                hit = self._preevicted.pop(chunk.chunk_id, None)
+                if hit is not None:  # moved bytes are counted when adopted
+                    self.stats.preevict_hits += 1
+                    self.stats.d2h_bytes += hit[0].numel() * hit[0].element_size()
         if hit is not None:  # issued ahead of time from the previous iteration's ledger
             d, done = hit
             self.stats.prefetch_hits += 1
@@ -556,7 +586,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._job_done(job)
 
     def _transfer(self, s: torch.Tensor, d: torch.Tensor, src: str, dst: str,
-                  prior: Optional["torch.cuda.Event"], after=None):
+                  prior: Optional["torch.cuda.Event"], after=None, count: bool = True):
         """cudaMemcpyAsync of a whole payload on the copy stream of its
         direction; returns the completion event consumers wait on
         (`wait_ready`).  D2H waits for the compute stream (the payload must be
@@ -586,9 +616,9 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         if src == GPU:
             s.record_stream(cs)
         with self._stats_lock:  # the host-Adam worker issues H2Ds too
-            if src == GPU:
+            if src == GPU and count:
                 self.stats.d2h_bytes += s.numel() * s.element_size()
-            if dst == GPU:
+            if dst == GPU and count:
                 self.stats.h2d_bytes += d.numel() * d.element_size()
             if t0 is not None:
                 self.stats.copy_events.append(("%s>%s" % (src, dst),
@@ -607,12 +637,72 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     # cross the ADAM event, and any D2H into / drop of the host copy discards
     # them).  The accounting fetch then adopts the in-flight buffer.
 
-    def set_prefetch_schedule(self, transfers) -> None:
+    def set_prefetch_schedule(self, transfers, samples=None, gpu_capacity: int = 0,
+                              adam_index: int = -1) -> None:
+        """Prefetch plan for the next iteration from this one's ledger.
+        ``adam_copy`` rows are never prefetched (their host source is what the
+        host Adam writes).  With the per-moment samples and the GPU pool's
+        capacity, ADAM's fetches are also placed early in the backward (see
+        ``_plan_adam_prefetch``); evictions of optimizer-state chunks before
+        ADAM become pre-evictions (``preevict``)."""
         sched: Dict[int, List[int]] = {}
         for t in transfers:
-            if t.src == CPU and t.dst == GPU and isinstance(t.chunk_id, int):
+            if t.src == CPU and t.dst == GPU and isinstance(t.chunk_id, int) \
+                    and t.reason != "adam_copy":
                 sched.setdefault((t.moment - 1) // 2, []).append(t.chunk_id)
         self._prefetch_sched = sched
+        self._preevict_ids = set()
+        self._adam_prefetch_at = {}
+        if adam_index < 0 or self.chunk_set is None:
+            return
+        adam_moment = 2 * adam_index + 1
+        if self.preevict:
+            for t in transfers:
+                if (t.src == GPU and t.dst == CPU and t.reason == "evict" and t.bytes > 0
+                        and isinstance(t.chunk_id, int) and t.moment < adam_moment
+                        and self.chunk_set.chunks[t.chunk_id].list_kind
+                        is not ChunkKind.PARAM_FP16):
+                    self._preevict_ids.add(t.chunk_id)
+        if self.early_adam_prefetch and samples and gpu_capacity > 0:
+            self._plan_adam_prefetch(sched.get(adam_index, ()), samples, gpu_capacity,
+                                     adam_index)
+
+    def _plan_adam_prefetch(self, ids, samples, capacity: int, adam_index: int) -> None:
+        """Move ADAM's fetches into the backward.  Fetch j (in walk order,
+        cumulative bytes B_j) is issued before the earliest event e at which
+        the last iteration's GPU usage stayed at most capacity - margin - B_j
+        from e up to ADAM: the activations the backward frees make the room
+        the accounting only uses at ADAM.  Only GPU-placed positions' chunks
+        (their host copies cannot change before ADAM)."""
+        plan = self._plan
+        if not ids or plan is None:
+            return
+        used: Dict[int, int] = {}
+        for smp in samples:
+            if smp.device == GPU:
+                used[smp.moment] = max(used.get(smp.moment, 0), smp.used_bytes)
+        if not used:
+            return
+        margin = int(self.adam_prefetch_margin * capacity)
+        first = min(used) // 2
+        # suffix maximum of the usage over [2e, 2*adam_index]
+        head: Dict[int, int] = {}
+        run = 0
+        for e in range(adam_index, first - 1, -1):
+            run = max(run, used.get(2 * e, 0), used.get(2 * e + 1, 0))
+            head[e] = capacity - margin - run
+        cum, e = 0, first
+        last = adam_index - max(self.prefetch_depth, 1)  # the rest: normal prefetch
+        for cid in ids:
+            chunk = self.chunk_set.chunks[cid]
+            if plan.device_of_position(chunk.position) != GPU:
+                continue
+            cum += chunk.bytes
+            while e <= last and head[e] < cum:
+                e += 1
+            if e > last:
+                break
+            self._adam_prefetch_at.setdefault(e, []).append(cid)
 
     def set_timeline(self, timeline) -> None:
         """Index the positions by their last BWD event (early gradient drain)."""
@@ -732,20 +822,33 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             self._prefetch_gathers(ev)
         if not self.prefetch_depth or not self._prefetch_sched:
             return
-        cs = self.chunk_set
+        for cid in self._adam_prefetch_at.get(ev.index, ()):
+            try:
+                if self._prefetch(cid):
+                    self.stats.adam_prefetch_early += 1
+            except torch.OutOfMemoryError:
+                # the room the ledger promised is not there physically: this
+                # chunk and the rest are fetched at ADAM as the ledger says
+                self._adam_prefetch_at = {}
+                self.stats.adam_prefetch_oom += 1
+                break
         for j in range(ev.index + 1, ev.index + 1 + self.prefetch_depth):
             for cid in self._prefetch_sched.get(j, ()):
-                if cid in self._prefetched or cid in self.payload[GPU]:
-                    continue
-                src = self.payload[CPU].get(cid)
-                if src is None:
-                    continue
-                chunk = cs.chunks[cid]
-                d = self._alloc_for_copy(chunk)
-                prior = self.ready.get((cid, CPU))
-                done = self._transfer(src, d, CPU, GPU, prior)
-                self._prefetched[cid] = (d, done)
-                self.stats.prefetch_issued += 1
+                self._prefetch(cid)
+
+    def _prefetch(self, cid: int) -> bool:
+        if cid in self._prefetched or cid in self.payload[GPU]:
+            return False
+        src = self.payload[CPU].get(cid)
+        if src is None or cid in self._jobs:
+            return False
+        chunk = self.chunk_set.chunks[cid]
+        d = self._alloc_for_copy(chunk)
+        prior = self.ready.get((cid, CPU))
+        done = self._transfer(src, d, CPU, GPU, prior)
+        self._prefetched[cid] = (d, done)
+        self.stats.prefetch_issued += 1
+        return True
 
     def _discard_prefetch(self, chunk: Chunk) -> None:
         hit = self._prefetched.pop(chunk.chunk_id, None)
@@ -784,8 +887,10 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     self.ready[key] = ev
                 self._retained[key] = t
                 t = None
-        if t is not None and device == CPU and chunk.list_kind is ChunkKind.PARAM_FP16:
+        if t is not None and device == CPU:
             self._give_host(t)
+        if device == GPU:
+            self._discard_preevict(cid)
         if t is not None and device == GPU:
             if cid in self._pending_ids:
                 self._flush_adam()  # K1 must update this payload before it is recycled
@@ -978,8 +1083,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.join_host_work()  # the previous step's host updates are complete
         cs = self.chunk_set
         self._plan = plan
-        for cid in list(self._prefetched):  # prefetches never cross the ADAM event
-            self._discard_prefetch(cs.chunks[cid])
+        for cid in list(self._prefetched):
+            # a prefetch crosses into ADAM only for a GPU-placed position (a
+            # host-placed one's host payload is what the host Adam rewrites)
+            if plan is None or plan.device_of_position(cs.chunks[cid].position) != GPU:
+                self._discard_prefetch(cs.chunks[cid])
         self._gather_prefetched.clear()     # (their Works are still in _inflight)
         self.wait_collectives()             # reduce-scatters into local chunks landed
         self._host_state = None
@@ -1074,8 +1182,14 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         triplet = cs.os_triplet(position)
         n = param.used_elems
         if device == GPU:
+            if self._preevict_ids and len(self._pending) >= self.preevict_batch \
+                    and not self._pending_ids.isdisjoint(self._preevict_ids):
+                # the pending positions' pre-evictions start behind this K1
+                # (their stale host copies were dropped by the walk's note_write)
+                self._flush_adam()
             for c in (param,) + triplet:
                 self.wait_ready(c, GPU)
+                self._discard_preevict(c.chunk_id)  # K1 rewrites it
             p16 = self.tensor(param, GPU)
             p32, m, v = (self.tensor(c, GPU) for c in triplet)
             self._pending.append((p16, p32, m, v, n))
@@ -1134,8 +1248,30 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             if self.adam_observer is not None:
                 self.adam_observer("post", self._pending)
             self.stats.adam_launch_items += len(self._pending)
+            if self._preevict_ids and not torch.cuda.is_current_stream_capturing():
+                for cid in sorted(self._pending_ids & self._preevict_ids):
+                    self._issue_preevict(cid)
         self._pending = []
         self._pending_ids = set()
+
+    def _issue_preevict(self, cid: int) -> None:
+        """D2H of an optimizer-state chunk K1 has just updated (enqueued), to
+        be adopted by the eviction the last iteration made before ADAM."""
+        chunk = self.chunk_set.chunks[cid]
+        if cid in self._preevicted or not self.has(chunk, GPU) or self.has(chunk, CPU):
+            return
+        d = self._alloc_d2h_dst(chunk)
+        done = self._transfer(self.payload[GPU][cid], d, GPU, CPU, None, count=False)
+        self._preevicted[cid] = (d, done)
+        self.stats.preevict_issued += 1
+
+    def _discard_preevict(self, cid: int) -> None:
+        hit = self._preevicted.pop(cid, None)
+        if hit is not None:
+            d, done = hit
+            self._give_host(d, done)  # reusable once its D2H has landed
+            self.stats.preevict_discarded += 1
+            self.stats.preevict_discarded_bytes += d.numel() * d.element_size()
 
     def _step_scalars_on_host(self):
         """Host copy of this step's scalars (waits for adam_prepare only)."""

@@ -396,7 +396,9 @@ class ChunkTrainer:
         else:  # the schedule is at its fixed point: prefetch next iteration's moves
             self.executor.prefetch_depth = self.prefetch_depth
             self.executor.gather_depth = self.gather_depth
-            self.executor.set_prefetch_schedule(report.transfers)
+            self.executor.set_prefetch_schedule(
+                report.transfers, report.samples, self.sim.pools[GPU].capacity_bytes,
+                self._events[-1].index)
         self.iteration += 1
         return loss.detach()
 

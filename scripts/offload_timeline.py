@@ -192,6 +192,7 @@ def main():
         "prefetch_issued", "prefetch_hits", "prefetch_discarded", "adam_prefetch_early",
         "adam_prefetch_oom", "preevict_issued", "preevict_hits", "preevict_discarded",
         "early_drains", "spec_issued", "spec_committed", "spec_cancelled")}
+    res["summary"]["alloc_retries"] = torch.cuda.memory_stats().get("num_alloc_retries", 0)
     print(json.dumps(res["summary"]))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
