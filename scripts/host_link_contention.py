@@ -26,7 +26,7 @@ from paper_2108_05818_b200 import _native as N  # noqa: E402
 from paper_2108_05818_b200 import kernels as K  # noqa: E402
 
 N16 = 64 << 20          # elements of one chunk
-REPS = 24
+REPS = 64
 
 
 def timed_copies(pairs, stream):
@@ -40,29 +40,28 @@ def timed_copies(pairs, stream):
     return a, b, sum(d.numel() * d.element_size() for d, _ in pairs)
 
 
-def run_case(name, dirs, host, dev, threads, adam_threads, dirty=False):
+def run_case(name, dirs, host, dev, items, adam_threads, dirty=False):
     streams = {"h2d": torch.cuda.Stream(), "d2h": torch.cuda.Stream()}
     stop = threading.Event()
+    started = threading.Event()
     rate = []
 
     def adam_loop():
-        items = [(torch.empty(N16, dtype=torch.float16, pin_memory=False).normal_(),
-                  torch.empty(N16).normal_(), torch.zeros(N16), torch.zeros(N16), N16)
-                 for _ in range(4)]
         prev = N.CsStepState(beta1_pow=1.0, beta2_pow=1.0, step=0, loss_scale=1.0)
         st = K.speculate_step_scalars(prev, K.AdamHyper(lr=1e-4))
         n = 0
         t0 = time.perf_counter()
         while not stop.is_set():
             K.adam_chunks_host(items, K.AdamHyper(lr=1e-4), st, adam_threads)
-            n += 4 * N16
+            n += sum(it[4] for it in items)
+            started.set()
         rate.append(n / (time.perf_counter() - t0) / 1e9)
 
     th = None
-    if threads:
+    if items:
         th = threading.Thread(target=adam_loop)
         th.start()
-        time.sleep(1.0)
+        started.wait()
     if dirty:
         for t in host:
             t.fill_(1.0)
@@ -78,7 +77,7 @@ def run_case(name, dirs, host, dev, threads, adam_threads, dirty=False):
     if th is not None:
         stop.set()
         th.join()
-    out = {"case": name, "gbs": res, "host_adam_threads": adam_threads if threads else 0}
+    out = {"case": name, "gbs": res, "host_adam_threads": adam_threads if items else 0}
     if rate:
         out["host_adam_gelem_per_s"] = round(rate[0], 2)
     print(json.dumps(out), flush=True)
@@ -94,10 +93,12 @@ def main():
     dev = [torch.empty(N16, dtype=torch.float16, device="cuda") for _ in range(4)]
     for t in host:
         t.zero_()
+    items = [(torch.empty(N16, dtype=torch.float16).fill_(1e-3), torch.full((N16,), 0.02),
+              torch.zeros(N16), torch.zeros(N16), N16) for _ in range(4)]
     for case, dirs in (("h2d", ["h2d"]), ("d2h", ["d2h"]), ("both", ["h2d", "d2h"])):
-        run_case(case + "_idle", dirs, host, dev, False, team)
-        run_case(case + "_dirty_dst", dirs, host, dev, False, team, dirty=True)
-        run_case(case + "_host_adam", dirs, host, dev, True, team)
+        run_case(case + "_idle", dirs, host, dev, None, team)
+        run_case(case + "_dirty_dst", dirs, host, dev, None, team, dirty=True)
+        run_case(case + "_host_adam", dirs, host, dev, items, team)
     print(json.dumps({"host_threads": ht, "worker_team": team}))
 
 
