@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--seq", type=int, default=1024)
     ap.add_argument("--vocab", type=int, default=50304)
     ap.add_argument("--dtype", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--embedding-weights", default="hbm", choices=["hbm", "host"],
+                    help="GPU-computed embedding state resident in HBM (default) or in host "
+                         "DRAM with the reference's weight round trip realised")
     ap.add_argument("--no-graph", action="store_true",
                     help="eager steps only (no CUDA-graph replay of the steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -543,7 +546,8 @@ def main():
     dtype = torch.float16 if args.dtype == "fp16" else torch.bfloat16
     trainer = ChunkTrainer(schema, PolicySpec(capacity_elems=args.cap), dtype=dtype, seed=0,
                            hyper=K.AdamHyper(lr=1e-4, betas=(0.9, 0.999), eps=1e-8),
-                           cuda_graph=not args.no_graph, graph_multi_rank=args.graph_dp)
+                           cuda_graph=not args.no_graph, graph_multi_rank=args.graph_dp,
+                           embedding_weights=args.embedding_weights)
     ex = trainer.executor
     B, S = args.batch, args.seq
     gen = torch.Generator().manual_seed(1000 + rank)
@@ -576,6 +580,8 @@ def main():
         ex.time_collectives = True
         ex.coll_log.clear()
     moved0 = ex.stats.h2d_bytes - ex.stats.prefetch_discarded_bytes + ex.stats.d2h_bytes
+    he = trainer.host_embedding
+    emb_moved0 = he.h2d_bytes + he.d2h_bytes if he is not None else 0
     reports0 = len(trainer.reports)
     launches0 = _native.launch_count()
     clocks = ClockSampler(local_rank)
@@ -606,6 +612,8 @@ def main():
     # moves none: it is only captured once the schedule moves no chunk)
     moved = (ex.stats.h2d_bytes - ex.stats.prefetch_discarded_bytes + ex.stats.d2h_bytes
              - moved0) / args.steps
+    emb_moved = ((he.h2d_bytes + he.d2h_bytes - emb_moved0) / args.steps
+                 if he is not None else 0)
     billed = [r.pcie_bytes for r in trainer.reports[reports0:reports0 + args.steps]]
     ex.record_k1 = False
     k1_ms = [a.elapsed_time(b) for a, b, _ in ex.k1_events]
@@ -698,10 +706,13 @@ def main():
         "pcie_per_step": {
             "ledger_billed_bytes": int(sum(billed) / max(len(billed), 1)),
             "physically_moved_chunk_bytes": int(moved),
+            "physically_moved_embedding_bytes": int(emb_moved),
             "ledger_rows_not_realized": trainer.ledger_rows_not_realized(),
+            "embedding_weights": trainer.embedding_weights,
             "note": "the reference bills a GPU-computed embedding's weights down at FWD and "
-                    "weight grads up at BWD (engine.py:214-219); here they stay resident in "
-                    "HBM, charged to the GPU pool (DESIGN.md section 7)"},
+                    "weight grads up at BWD (engine.py:214-219); by default they stay resident "
+                    "in HBM, charged to the GPU pool; --embedding-weights host realises the "
+                    "round trip (DESIGN.md section 7)"},
         "gpu_resident_non_chunked_bytes": trainer.gpu_resident_bytes,
         "non_model": "measured" if trainer.tracer is not None else "analytic",
         "host_threads": trainer.host_threads,

@@ -35,7 +35,7 @@ class HostEmbedding:
     """Host-resident embedding weights + the host operator; one per trainer."""
 
     def __init__(self, vocab: int, seq_len: int, hidden: int, dtype: torch.dtype,
-                 device: torch.device, threads: int = 0):
+                 device: torch.device, threads: int = 0, device_compute: bool = False):
         self.vocab, self.seq_len, self.hidden = vocab, seq_len, hidden
         self.dtype, self.device, self.threads = dtype, torch.device(device), threads
         pin = dict(pin_memory=True)
@@ -56,6 +56,18 @@ class HostEmbedding:
         self.host_seconds = 0.0
         # a leaf that requires grad, so autograd calls the host backward
         self.anchor = torch.zeros(0, device=self.device, requires_grad=True)
+        #: GPU-computed embedding with host-resident weights and optimizer
+        #: state (the reference's GPU branch realised, `engine.py:214-219`):
+        #: the model computes on ``device_params`` = [wte] (the HBM copy of
+        #: the V x H weights the reference bills, `chunks.py:204-224`, shared
+        #: with a tied LM head; the small wpe is not billed and stays an HBM
+        #: parameter updated by K1); the gradient goes D2H at ADAM, the host
+        #: Adam updates the host state, the new weights go H2D for the next
+        #: forward (``h2d_done``)
+        self.device_compute = device_compute
+        self.device_params: List[torch.nn.Parameter] = []
+        self.d2h_done: Optional[torch.cuda.Event] = None
+        self.h2d_done: Optional[torch.cuda.Event] = None
 
     def load(self, wte32: torch.Tensor, wpe32: torch.Tensor) -> None:
         """Initial weights (fp32, any device): masters, and the fp16 copies
@@ -84,13 +96,40 @@ class HostEmbedding:
     def forward(self, tokens: torch.Tensor) -> torch.Tensor:
         return _HostEmbeddingFn.apply(tokens, self, self.anchor)
 
+    def drain_grads(self, grads, d2h: torch.cuda.Stream, compute: torch.cuda.Stream) -> None:
+        """D2H of the device weight gradients over the host fp16 weights (the
+        host copy of the grad overwrite), ordered after ``compute``."""
+        d2h.wait_stream(compute)
+        with torch.cuda.stream(d2h):
+            for host, g in zip(self._host_weights(), grads):
+                host.view(-1).copy_(g.reshape(-1), non_blocking=True)
+                g.record_stream(d2h)
+                self.d2h_bytes += host.numel() * host.element_size()
+            self.d2h_done = torch.cuda.Event()
+            self.d2h_done.record(d2h)
+
+    def upload(self, h2d: torch.cuda.Stream, compute: torch.cuda.Stream) -> None:
+        """H2D of the updated host weights into the device copies, after every
+        device read of the gradients they held (K2 on ``compute``, the D2H)."""
+        h2d.wait_stream(compute)
+        h2d.wait_event(self.d2h_done)
+        with torch.cuda.stream(h2d):
+            for host, p in zip(self._host_weights(), self.device_params):
+                p.data.view(-1).copy_(host.view(-1), non_blocking=True)
+                self.h2d_bytes += host.numel() * host.element_size()
+            self.h2d_done = torch.cuda.Event()
+            self.h2d_done.record(h2d)
+
+    def _host_weights(self):
+        return (self.wte,) if self.device_compute else (self.wte, self.wpe)
+
     def adam_items(self):
         """(g16/p16, p32, m, v, n) host items for ``cs_adam_chunks_host``."""
         return [(p16.view(-1), p32.view(-1), m.view(-1), v.view(-1), p16.numel())
-                for p16, (p32, m, v) in zip((self.wte, self.wpe), self.state)]
+                for p16, (p32, m, v) in zip(self._host_weights(), self.state)]
 
     def grad_items(self):
-        return [(p16.view(-1), p16.numel()) for p16 in (self.wte, self.wpe)]
+        return [(p16.view(-1), p16.numel()) for p16 in self._host_weights()]
 
 
 class _HostEmbeddingFn(torch.autograd.Function):

@@ -1112,7 +1112,18 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 self.wait_ready(chunk, CPU)
                 host_items.append((self.tensor(chunk, CPU), n))
         he = self.host_embedding
-        if he is not None:
+        dev_emb = he is not None and he.device_compute
+        drained = []
+        if dev_emb:  # GPU-computed embedding, weights and optimizer state in host DRAM
+            for param in he.device_params:
+                g = param.data if grad_in_data(param) else param.grad
+                if g is None:
+                    raise RuntimeError("embedding has no gradient at ADAM")
+                if self.comm is not None and self.comm.world > 1:
+                    self.comm.all_reduce_avg(g)
+                emb_grads.append((g, g.numel()))
+                drained.append(g)
+        if he is not None and not dev_emb:
             if not he.grads_ready:
                 raise RuntimeError("host embedding has no gradient at ADAM")
             if self.comm is not None and self.comm.world > 1:
@@ -1123,7 +1134,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         host_extra = 0.0
         if self.comm is None or self.comm.rank == 0:
             dev_items += emb_grads  # replicated after the all-reduce: count once
-            if he is not None:
+            if he is not None and not dev_emb:
                 if self.comm is None or self.comm.world == 1:
                     host_extra = he.grad_sumsq  # computed by the scatter, hit rows only
                 else:                           # averaged over ranks since: recount
@@ -1133,6 +1144,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.partials[-1:].fill_(host)
         K.grad_sumsq(dev_items, self.partials[:-1], dtype=self.dtype)
         K.sumsq_finalize(self.partials, self.state)
+        if dev_emb:  # the weight gradients go up (`engine.py:214-219`, billed at BWD)
+            he.drain_grads(drained, self.d2h_stream, self.compute)
+            for param in he.device_params:
+                if grad_in_data(param):
+                    mark_grad_in_data(param, False)
+                else:
+                    param.grad = None
         if self.comm is not None and self.comm.world > 1:
             self.comm.all_reduce_sum(self.state.sumsq())
         K.adam_prepare(self.state, self.hyper, max_grad_norm=self.max_grad_norm,
@@ -1286,9 +1304,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._gather_sched, self._gather_log = sched, []
         self._flush_adam()
         he = self.host_embedding
-        if he is not None:  # CPU-placed embedding: host Adam overlaps K1
+        if he is not None:  # host-resident embedding state: host Adam overlaps K1
             if self._host_state is None:
                 self._host_state = self._step_scalars_on_host()
+            if he.device_compute:
+                he.d2h_done.synchronize()
             t0 = time.perf_counter()
             K.adam_chunks_host(he.adam_items(), self.hyper, self._host_state,
                                self.host_threads)
@@ -1297,6 +1317,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 self.stats.host_adam_seconds += dt
             he.host_seconds += dt
             he.grads_ready = False
+            if he.device_compute:  # weights down for the next forward (billed at FWD)
+                he.upload(self.copy_stream, self.compute)
         for pos in list(self._spec):  # never reached its ADAM turn: recycle
             fut, _, shadow, _ = self._spec.pop(pos)
             if not fut.cancel():

@@ -105,7 +105,8 @@ class ChunkTrainer:
                  async_host_adam: Optional[bool] = None,
                  comm=None, bind_host: Optional[bool] = None,
                  speculative_host_adam: Optional[bool] = None,
-                 graph_multi_rank: Optional[bool] = None):
+                 graph_multi_rank: Optional[bool] = None,
+                 embedding_weights: str = "hbm"):
         if not torch.cuda.is_available():
             raise RuntimeError("ChunkTrainer needs a CUDA device (B200); there is no CPU path")
         self.device = torch.device(device or "cuda:%d" % torch.cuda.current_device())
@@ -155,12 +156,24 @@ class ChunkTrainer:
             raise ValueError("embedding_placement must be 'plan', 'cpu' or 'gpu'")
         if embedding_placement == CPU and not untied_head:
             raise ValueError("a CPU-placed embedding needs an untied LM head (untied_head=True)")
+        # a GPU-computed embedding's weights and optimizer state: resident in
+        # HBM and updated by K1 ("hbm", the default), or in pinned host DRAM
+        # with the reference's round trip realised ("host": weights down for
+        # the forward, weight gradients up, host Adam; `engine.py:214-219`)
+        if embedding_weights not in ("hbm", "host"):
+            raise ValueError("embedding_weights must be 'hbm' or 'host'")
+        dev_emb_host = embedding_placement == GPU and embedding_weights == "host"
+        self.embedding_weights = "host" if embedding_placement == CPU else embedding_weights
         V, H, S = schema.vocab, schema.hidden_dim, schema.seq_len
         # non-chunked parameters that live in HBM for the whole run: fp16/bf16
         # weights (their gradients overwrite them) + fp32 master / m / v
-        gpu_resident_elems = (0 if embedding_placement == CPU else (V + S) * H) + \
-            (V * H if untied_head else 0)
-        self.gpu_resident_bytes = gpu_resident_elems * (2 + 12)
+        if embedding_placement == CPU:
+            emb_bytes = 0
+        elif dev_emb_host:  # wte's HBM copy (fp16 only); wpe with its state
+            emb_bytes = V * H * 2 + S * H * 14
+        else:
+            emb_bytes = (V + S) * H * 14
+        self.gpu_resident_bytes = emb_bytes + (V * H * 14 if untied_head else 0)
         if non_model == "auto":
             non_model = "measured" if hardware is None and non_model_fn is None else "analytic"
         if hardware is None:
@@ -209,11 +222,15 @@ class ChunkTrainer:
             self.model = ReferenceShapedGPT(schema, dtype=dtype, placeholders=True,
                                             fused=fused_ops, untied_head=untied_head)
         self.host_embedding = None
-        if host_emb:
+        if host_emb or dev_emb_host:
             self.host_embedding = HostEmbedding(schema.vocab, schema.seq_len,
                                                 schema.hidden_dim, dtype, self.device,
-                                                threads=host_threads)
-            self.model.host_embedding = self.host_embedding
+                                                threads=host_threads,
+                                                device_compute=dev_emb_host)
+            if host_emb:
+                self.model.host_embedding = self.host_embedding
+            else:
+                self.host_embedding.device_params = [self.model.embedding_parameters()[0]]
             ex.host_embedding = self.host_embedding
         self.shapes = reference_tensor_shapes(schema)
         if fused_ops and K.layernorm_supported(schema.hidden_dim):
@@ -227,11 +244,16 @@ class ChunkTrainer:
         # GPU-placed, else the (untied) LM head
         emb = []
         V, H = schema.vocab, schema.hidden_dim
+        # (param, shape, seed offset): wte 0, wpe 1, untied head 2 — the same
+        # values wherever each one lives
+        wte_p, wpe_p = self.model.embedding_parameters()
         gpu_params = ([] if host_emb else
-                      list(zip(self.model.embedding_parameters(), [(V, H), (schema.seq_len, H)])))
+                      [(wpe_p, (schema.seq_len, H), 1)] if dev_emb_host else
+                      [(wte_p, (V, H), 0), (wpe_p, (schema.seq_len, H), 1)])
         if untied_head:
-            gpu_params.append((self.model.lm_head, (V, H)))
-        for p, shape in gpu_params:
+            gpu_params.append((self.model.lm_head, (V, H), 2))
+        self._emb_seed_offsets = [k for _, _, k in gpu_params]
+        for p, shape, _ in gpu_params:
             master = torch.empty(shape, dtype=torch.float32, device=self.device)
             emb.append((p, master, torch.zeros_like(master), torch.zeros_like(master)))
         ex.attach(self.sim.chunk_set, self.sim.partition, rank,
@@ -298,11 +320,10 @@ class ChunkTrainer:
                                                                         generator=gen))
             self.host_embedding.load(*w)
             del w
-            first = 2
-        else:
-            first = 0
-        for k, (p, master, m, v) in enumerate(emb):
-            gen.manual_seed(seed * 1_000_003 + n_chunked + first + k)
+            for p in self.host_embedding.device_params:  # wte: the HBM copy the GPU reads
+                p.data = self.host_embedding.wte.to(self.device)
+        for k, (p, master, m, v) in zip(self._emb_seed_offsets, emb):
+            gen.manual_seed(seed * 1_000_003 + n_chunked + k)
             master.normal_(0.0, 0.02, generator=gen)
             p.data = torch.empty(master.shape, dtype=self.dtype, device=self.device)
             K.cast_pack([(p.data.view(-1), 0, master.view(-1), master.numel())])
@@ -367,6 +388,9 @@ class ChunkTrainer:
         eng.begin_iteration(self.iteration, warm,
                             self.sim._plan_builder() if warm else None, self.sim.local)
         self._check()
+        he = self.host_embedding
+        if he is not None and he.h2d_done is not None:  # last ADAM's weights have landed
+            torch.cuda.current_stream(self.device).wait_event(he.h2d_done)
         try:
             t0 = time.perf_counter()
             inp, tgt = tokens[:, :-1], tokens[:, 1:]
@@ -498,7 +522,8 @@ class ChunkTrainer:
             loss = self.step(self._static_tokens)
         else:
             tokens = tokens_host.to(self.device, non_blocking=True)
-            if self.host_embedding is not None:  # the host lookup reads these, no D2H
+            if self.host_embedding is not None and not self.host_embedding.device_compute:
+                # the host lookup reads these, no D2H
                 self.host_embedding.host_tokens = tokens_host[:, :-1]
             loss = self.step(tokens)
         return PendingLoss(loss)
@@ -537,14 +562,17 @@ class ChunkTrainer:
         at BWD (`engine.py:214-219`) because its fp16 weights live in host
         memory (`chunks.py:204-224`, `scenario.py:133`); here a GPU-computed
         embedding keeps weights, gradients and optimizer state resident in
-        HBM (charged to the GPU pool, ``gpu_resident_bytes``), so those rows
-        have no copy behind them.  A CPU-computed embedding ships exactly the
-        activation rows it is billed (realized)."""
+        HBM by default (charged to the GPU pool, ``gpu_resident_bytes``), so
+        those rows have no copy behind them; ``embedding_weights="host"``
+        realises them (host-resident state, one weight H2D and one gradient
+        D2H per step).  A CPU-computed embedding ships exactly the activation
+        rows it is billed (realized)."""
         r = report if report is not None else (self.reports[-1] if self.reports else None)
         if r is None:
             return {}
         emb = sum(t.bytes for t in r.transfers if t.chunk_id == "embedding")
-        realized = self.embedding_placement == CPU == self.sim.engine.embedding_device
+        realized = (self.embedding_placement == self.sim.engine.embedding_device
+                    and (self.embedding_placement == CPU or self.embedding_weights == "host"))
         return {} if realized or emb == 0 else {"embedding": emb}
 
     def step_state(self):

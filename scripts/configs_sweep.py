@@ -44,6 +44,10 @@ CONFIGS = {
     "12b_ckpt_analytic": dict(layers=60, hidden=4096, heads=32, batch=8, cap=64 * MI,
                               os="auto", ckpt=True, nm="analytic"),
     "1b_os_cpu": dict(layers=20, hidden=2048, heads=16, batch=32, cap=64 * MI, os="cpu"),
+    # the bench configuration with the reference's GPU-embedding round trip
+    # realised (weights and optimizer state in host DRAM, host Adam)
+    "1b_emb_host": dict(layers=20, hidden=2048, heads=16, batch=32, cap=64 * MI, os="auto",
+                        embw="host"),
     "1b_b16_emb_plan": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
                             os="auto", untied=True),
     "1b_b16_emb_gpu": dict(layers=20, hidden=2048, heads=16, batch=16, cap=64 * MI,
@@ -74,6 +78,7 @@ def run_one(name: str) -> dict:
                       embedding_placement=c.get("emb", "plan"),
                       untied_head=bool(c.get("untied", False)),
                       non_model=c.get("nm", "auto"),
+                      embedding_weights=c.get("embw", "hbm"),
                       prefetch_depth=int(os.environ.get("CS_PREFETCH_DEPTH", "2")))
     t_init = time.perf_counter() - t_init
     gen = torch.Generator().manual_seed(3)
