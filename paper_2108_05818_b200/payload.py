@@ -344,6 +344,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.time_collectives = False
         self.coll_log: List[tuple] = []
         self._free_host: Dict[tuple, List[tuple]] = {}  # (dtype, numel) -> [(tensor, event)]
+        #: pinned buffer (data_ptr) -> completion event of the last H2D that read it
+        self._host_reads: Dict[int, "torch.cuda.Event"] = {}
+        #: HBM slab (data_ptr) -> {side stream: completion event of its last copy there}
+        self._side_use: Dict[int, Dict[int, "torch.cuda.Event"]] = {}
+        self._host_read_events = os.environ.get("CS_HOST_READ_EVENTS", "1") != "0"
         self._stats_lock = threading.Lock()
         #: CPU-placed embedding operator (embedding.HostEmbedding) or None
         self.host_embedding = None
@@ -443,16 +448,17 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         """HBM destination of an H2D copy, taken from the copy stream's pool so
         the copy need not wait for the compute stream; the compute stream is
         registered as a user (it consumes the payload after `wait_ready`)."""
-        d = self.slabs.take(chunk.capacity_elems, self._elem_dtype(chunk), self.copy_stream)
-        d.record_stream(self.compute)
-        return d
+        return self.slabs.take(chunk.capacity_elems, self._elem_dtype(chunk), self.copy_stream)
+
+    def _side_events(self, t: torch.Tensor):
+        return list(self._side_use.pop(t.data_ptr(), {}).values())
 
     def _release(self, cid: int, t: torch.Tensor) -> None:
         """A GPU payload leaves the executor: back to the slab pool once the
         work already enqueued on it (incl. a collective writing it) is done."""
         if cid in self._coll_work:
             self._wait_collective(cid)
-        self.slabs.give(t)
+        self.slabs.give(t, self._side_events(t))
 
     def tensor(self, chunk: Chunk, device: str) -> torch.Tensor:
         self._join(chunk.chunk_id)
@@ -613,8 +619,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             d.copy_(s, non_blocking=True)
             done = torch.cuda.Event(enable_timing=self.time_copies)
             done.record(cs)
-        if src == GPU:
-            s.record_stream(cs)
+        if src == CPU:
+            self._host_reads[s.data_ptr()] = done
+        for t in ((s,) if src == GPU else ()) + ((d,) if dst == GPU else ()):
+            if self.slabs.owns(t):  # handed back to the pool with the slab (``_release``)
+                self._side_use.setdefault(t.data_ptr(), {})[id(cs)] = done
+            else:
+                t.record_stream(cs)
         with self._stats_lock:  # the host-Adam worker issues H2Ds too
             if src == GPU and count:
                 self.stats.d2h_bytes += s.numel() * s.element_size()
@@ -853,7 +864,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     def _discard_prefetch(self, chunk: Chunk) -> None:
         hit = self._prefetched.pop(chunk.chunk_id, None)
         if hit is not None:
-            self.slabs.give(hit[0])
+            self.slabs.give(hit[0], self._side_events(hit[0]))
             self.stats.prefetch_discarded += 1
             self.stats.prefetch_discarded_bytes += hit[0].numel() * hit[0].element_size()
 
@@ -888,7 +899,10 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 self._retained[key] = t
                 t = None
         if t is not None and device == CPU:
-            self._give_host(t)
+            # reusable once the last copy that read it has landed -- not the
+            # H2D stream's tail, which at ADAM holds every fetch of the walk
+            ev = self._host_reads.pop(t.data_ptr(), None)
+            self._give_host(t, ev if self._host_read_events else None)
         if device == GPU:
             self._discard_preevict(cid)
         if t is not None and device == GPU:

@@ -11,8 +11,12 @@ caching allocator (whose out-of-memory path frees every cached block with a
 device sync and retries).
 
 Reuse is stream-ordered without host syncs: ``give`` records an event on
-every stream that may have touched the slab (compute, H2D, D2H) and
-``take`` makes the taking stream wait on them.  Inside a CUDA-graph capture
+the compute stream and takes the completion events of the slab's last copy
+on each side stream (the executor tracks them per slab), and ``take`` makes
+the taking stream wait on them.  Events at the side streams' *tails* would
+also be safe but make a taker wait for every unrelated copy queued there
+(at ADAM the H2D stream holds the whole walk's fetches, after it the D2H
+stream the pre-evictions).  Inside a CUDA-graph capture
 the pool is bypassed (events recorded outside a capture cannot be waited on
 inside it).
 
@@ -29,7 +33,7 @@ Two rules keep HBM shared with the model's activations:
 """
 
 import os
-from typing import Dict, List, Sequence, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import torch
 
@@ -67,29 +71,47 @@ class SlabPool:
             ev = torch.cuda.Event()
             ev.record(home)
             stream.wait_event(ev)
-            t.record_stream(stream)
+            # no record_stream: the side stream's use is handed back with the
+            # slab (``give(side_events=...)``), which orders its eventual free
         self._owned[t.data_ptr()] = key
         self.allocs += 1
         return t
 
-    def give(self, t: torch.Tensor) -> bool:
+    def owns(self, t: torch.Tensor) -> bool:
+        key = self._owned.get(t.data_ptr())
+        return key is not None and t.numel() == key[1] and t.dtype == key[0]
+
+    def give(self, t: torch.Tensor, side_events: Optional[Sequence] = None) -> bool:
         """Return a slab obtained from :meth:`take` (any other tensor: False).
-        Work already enqueued that uses it finishes before its next user."""
+        Work already enqueued that uses it finishes before its next user:
+        the compute stream's work as enqueued now, the side streams' work up
+        to ``side_events`` (the completion of the slab's last copy on each;
+        None: up to their tails)."""
         key = self._owned.get(t.data_ptr())
         if key is None or t.numel() != key[1] or t.dtype != key[0] \
                 or torch.cuda.is_current_stream_capturing():
             return False
         lst = self._free.setdefault(key, [])
+        home = self.streams[0]
         if len(lst) >= self.max_free:  # back to the caching allocator (compute pool)
             del self._owned[t.data_ptr()]
-            for s in self.streams[1:]:
-                t.record_stream(s)
+            if side_events is None:
+                for s in self.streams[1:]:
+                    t.record_stream(s)
+            else:  # free in compute order once its own copies have landed
+                for ev in side_events:
+                    home.wait_event(ev)
             return True
-        events = []
-        for s in self.streams:
+        if side_events is None:
+            events = []
+            for s in self.streams:
+                ev = torch.cuda.Event()
+                ev.record(s)
+                events.append(ev)
+        else:
             ev = torch.cuda.Event()
-            ev.record(s)
-            events.append(ev)
+            ev.record(home)
+            events = [ev] + list(side_events)
         lst.append((t, events))
         self.gives += 1
         return True

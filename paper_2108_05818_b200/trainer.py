@@ -185,7 +185,7 @@ class ChunkTrainer:
             # measured warm-up tracer R - C already holds the activations and
             # library workspaces, so less slack is kept than with the
             # reference's analytic activation model.
-            frac = 0.93 if non_model == "measured" else 0.9
+            frac = float(os.environ.get("CS_GPU_FRAC", 0.93 if non_model == "measured" else 0.9))
             hardware = HardwareSpec(gpu_count=nproc,
                                     gpu_bytes=int(total * frac) - self.gpu_resident_bytes,
                                     cpu_bytes=int(_host_ram_bytes() * 0.8))

@@ -95,7 +95,7 @@ def run_one(name: str) -> dict:
         tr.step(toks[extra % 2])
         extra += 1
     torch.cuda.synchronize()
-    steps = 3 if slow else 6
+    steps = int(os.environ.get("CS_SWEEP_STEPS", 3 if slow else 6))
     hs0 = torch.cuda.host_memory_stats()
     retries0 = torch.cuda.memory_stats().get("num_alloc_retries", 0)
     ph0 = dict(tr.phase_seconds)

@@ -13,6 +13,7 @@ import argparse
 import json
 import os
 import sys
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -93,22 +94,79 @@ def timeline(tr, toks):
         tr.step(toks[i % 2])
     tr.finish_host_work()
     torch.cuda.synchronize()
+    for i in range(2):  # steady state: the host work of the previous step still runs
+        tr.step(toks[i % 2])
+    rs0 = ex._run_spec
+
+    def run_spec(waits, item_in, item_out, state):
+        t = time.perf_counter()
+        rs0(waits, item_in, item_out, state)
+        jobs.append(("spec", t, time.perf_counter()))
+
+    blocks = []
+    j0 = ex._join
+
+    def join(cid):
+        t = time.perf_counter()
+        j0(cid)
+        dt = time.perf_counter() - t
+        if dt > 1e-3:
+            blocks.append(("join", cid, t, t + dt))
+
+    wr0 = ex.wait_ready
+
+    def wait_ready(chunk, device):
+        t = time.perf_counter()
+        wr0(chunk, device)
+        dt = time.perf_counter() - t
+        if dt > 1e-3:
+            blocks.append(("wait_ready_" + device, chunk.chunk_id, t, t + dt))
+
     eng.start_event, eng.finish_event, ex._run_host_adam = start, finish, run_host_adam
+    ex._run_spec = run_spec
+    ex._join, ex.wait_ready = join, wait_ready
+    retries0 = torch.cuda.memory_stats().get("num_alloc_retries", 0)
     ex.stats.copy_events.clear()
+    samples = []
+    stop = threading.Event()
+    main_id = threading.get_ident()
+
+    def sampler():  # poor man's profiler of the enqueueing thread
+        while not stop.is_set():
+            f = sys._current_frames().get(main_id)
+            stack = []
+            while f is not None and len(stack) < 12:
+                stack.append("%s:%d:%s" % (os.path.basename(f.f_code.co_filename), f.f_lineno,
+                                           f.f_code.co_name))
+                f = f.f_back
+            samples.append((time.perf_counter(), stack))
+            time.sleep(0.002)
+
+    th = threading.Thread(target=sampler, daemon=True)
     z = torch.cuda.Event(enable_timing=True)
     z.record()
     hz = time.perf_counter()
+    th.start()
     tr.step(toks[0])
     tr.step(toks[1])  # the next step's forward shows when the updated params land
     tr.finish_host_work()
     torch.cuda.synchronize()
+    stop.set()
+    th.join()
     eng.start_event, eng.finish_event, ex._run_host_adam = s0, f0, r0
+    ex._run_spec = rs0
+    ex._join, ex.wait_ready = j0, wr0
+    retries = torch.cuda.memory_stats().get("num_alloc_retries", 0) - retries0
     ev = [(i, n, k, round((h - hz) * 1e3, 2), round(z.elapsed_time(e), 2))
           for i, n, k, h, e in marks]
     copies = [(name, round(z.elapsed_time(a), 2), round(z.elapsed_time(b), 2), nb)
               for name, nb, a, b in ex.stats.copy_events]
     host = [(cid, round((a - hz) * 1e3, 2), round((b - hz) * 1e3, 2)) for cid, a, b in jobs]
-    return {"events": ev, "copies": copies, "host_adam": host}
+    blk = [(k, cid, round((a - hz) * 1e3, 2), round((b - hz) * 1e3, 2)) for k, cid, a, b in blocks]
+    smp = [(round((t - hz) * 1e3, 1), st) for t, st in samples]
+    return {"events": ev, "copies": copies, "host_adam": host, "host_blocks": blk,
+            "main_thread_samples": smp,
+            "alloc_retries_recorded": retries}
 
 
 def _busy(windows):

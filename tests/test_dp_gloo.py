@@ -57,7 +57,10 @@ def _fake_grad(numel: int, rank: int) -> np.ndarray:
 class _NoSlabs:
     """Host double of the HBM slab pool: payloads are plain host tensors."""
 
-    def give(self, t):
+    def give(self, t, side_events=None):
+        return False
+
+    def owns(self, t):
         return False
 
     def free_tensors(self):
