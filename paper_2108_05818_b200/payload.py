@@ -101,6 +101,42 @@ class ChunkComm:
         dist.all_reduce(t, op=dist.ReduceOp.AVG, group=self.group)
 
 
+def plan_early_fetches(fetches, used, capacity: int, margin: int, adam_index: int,
+                       last_event: int) -> Dict[int, List[int]]:
+    """Events at which to issue ADAM's fetches ahead of the ledger.
+
+    ``fetches``: (chunk id, bytes) in the ADAM walk's order; ``used``:
+    (moment, GPU pool bytes in use) of the last iteration's samples (the grid
+    puts moment 2e before event e and 2e+1 during it, `model.py:209-214`).
+    Fetch j, with cumulative bytes B_j, goes before the earliest event e whose
+    usage from moment 2e up to ADAM stayed at most capacity - margin - B_j:
+    holding every earlier-issued fetch as well, nothing the last iteration
+    used before ADAM would have been short of room.  Fetches that would land
+    after ``last_event`` (and every one after them: the walk's order is kept)
+    are left to the ordinary prefetch."""
+    peak: Dict[int, int] = {}
+    for m, b in used:
+        peak[m] = max(peak.get(m, 0), b)
+    if not peak or not fetches:
+        return {}
+    first = min(peak) // 2
+    head: Dict[int, int] = {}  # capacity - margin - max usage over [2e, 2*adam_index + 1]
+    run = 0
+    for e in range(adam_index, first - 1, -1):
+        run = max(run, peak.get(2 * e, 0), peak.get(2 * e + 1, 0))
+        head[e] = capacity - margin - run
+    out: Dict[int, List[int]] = {}
+    cum, e = 0, first
+    for cid, nbytes in fetches:
+        cum += nbytes
+        while e <= last_event and head[e] < cum:
+            e += 1
+        if e > last_event:
+            break
+        out.setdefault(e, []).append(cid)
+    return out
+
+
 class _PriorityWorker:
     """One host thread running host-Adam jobs, lowest position first among
     the jobs whose inputs are ready.
@@ -679,41 +715,18 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                                      adam_index)
 
     def _plan_adam_prefetch(self, ids, samples, capacity: int, adam_index: int) -> None:
-        """Move ADAM's fetches into the backward.  Fetch j (in walk order,
-        cumulative bytes B_j) is issued before the earliest event e at which
-        the last iteration's GPU usage stayed at most capacity - margin - B_j
-        from e up to ADAM: the activations the backward frees make the room
-        the accounting only uses at ADAM.  Only GPU-placed positions' chunks
-        (their host copies cannot change before ADAM)."""
+        """Move ADAM's fetches of GPU-placed positions (their host copies
+        cannot change before ADAM) into the backward: ``plan_early_fetches``."""
         plan = self._plan
         if not ids or plan is None:
             return
-        used: Dict[int, int] = {}
-        for smp in samples:
-            if smp.device == GPU:
-                used[smp.moment] = max(used.get(smp.moment, 0), smp.used_bytes)
-        if not used:
-            return
-        margin = int(self.adam_prefetch_margin * capacity)
-        first = min(used) // 2
-        # suffix maximum of the usage over [2e, 2*adam_index]
-        head: Dict[int, int] = {}
-        run = 0
-        for e in range(adam_index, first - 1, -1):
-            run = max(run, used.get(2 * e, 0), used.get(2 * e + 1, 0))
-            head[e] = capacity - margin - run
-        cum, e = 0, first
-        last = adam_index - max(self.prefetch_depth, 1)  # the rest: normal prefetch
-        for cid in ids:
-            chunk = self.chunk_set.chunks[cid]
-            if plan.device_of_position(chunk.position) != GPU:
-                continue
-            cum += chunk.bytes
-            while e <= last and head[e] < cum:
-                e += 1
-            if e > last:
-                break
-            self._adam_prefetch_at.setdefault(e, []).append(cid)
+        chunks = [self.chunk_set.chunks[cid] for cid in ids]
+        fetches = [(c.chunk_id, c.bytes) for c in chunks
+                   if plan.device_of_position(c.position) == GPU]
+        used = [(smp.moment, smp.used_bytes) for smp in samples if smp.device == GPU]
+        self._adam_prefetch_at = plan_early_fetches(
+            fetches, used, capacity, int(self.adam_prefetch_margin * capacity), adam_index,
+            adam_index - max(self.prefetch_depth, 1))
 
     def set_timeline(self, timeline) -> None:
         """Index the positions by their last BWD event (early gradient drain)."""
