@@ -380,6 +380,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self.time_collectives = False
         self.coll_log: List[tuple] = []
         self._free_host: Dict[tuple, List[tuple]] = {}  # (dtype, numel) -> [(tensor, event)]
+        self._free_host_bytes = 0
         #: pinned buffer (data_ptr) -> completion event of the last H2D that read it
         self._host_reads: Dict[int, "torch.cuda.Event"] = {}
         #: HBM slab (data_ptr) -> {side stream: completion event of its last copy there}
@@ -455,26 +456,29 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
     # are served this way (the host never writes these buffers before the
     # D2H that fills them has completed).
 
-    HOST_FREE_PER_KIND = 256
+    #: pinned bytes kept for reuse; beyond it a dropped buffer goes back to
+    #: PyTorch's pinned cache (the accounting's CPU pool no longer counts it)
+    HOST_FREE_BYTES = int(float(os.environ.get("CS_HOST_FREE_GB", "8")) * 2**30)
 
     def _give_host(self, t: torch.Tensor, ev: Optional["torch.cuda.Event"] = None) -> None:
         """``ev``: the last device work on ``t`` (default: whatever the H2D
         stream has enqueued so far, i.e. every copy that may still read it)."""
-        if not t.is_pinned():
+        nbytes = t.numel() * t.element_size()
+        if not t.is_pinned() or self._free_host_bytes + nbytes > self.HOST_FREE_BYTES:
             return
         lst = self._free_host.setdefault((t.dtype, t.numel()), [])
-        if len(lst) >= self.HOST_FREE_PER_KIND:
-            return
         if ev is None and self.copy_stream is not None:
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
         lst.append((t, ev))
+        self._free_host_bytes += nbytes
 
     def _alloc_d2h_dst(self, chunk: Chunk) -> torch.Tensor:
         """Pinned host destination of a D2H copy (see ``_give_host``)."""
         lst = self._free_host.get((self._elem_dtype(chunk), chunk.capacity_elems))
         if lst:
             t, ev = lst.pop()
+            self._free_host_bytes -= t.numel() * t.element_size()
             if ev is not None:
                 self.d2h_stream.wait_event(ev)
             return t
