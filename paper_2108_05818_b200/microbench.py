@@ -12,13 +12,16 @@ see the kernel alone, cold.  Sizes below ~4M elements are latency-bound
 labelled so; the roofline fraction is meaningful from 16M elements up.
 
 CPU arms (SURVEY §8d CPU baseline items 2-3), same element counts, same
-28 B/element of algorithmic traffic, host DRAM:
+algorithmic bytes per element, host DRAM:
 
 * ``cpu_torch_fused``: torch-CPU fused Adam (``torch.optim.Adam(fused=True)``
   over the fp32 master) with the chunk path's casts — fp16 gradients widened
   to fp32 before, the fp16 parameter copy narrowed after;
 * ``cpu_host_k1``: this build's own host K1 (``cs_adam_chunks_host``, AVX2 +
-  OpenMP), the kernel that runs CPU-placed optimizer triplets.
+  OpenMP), the kernel that runs CPU-placed optimizer triplets;
+* ``cpu_torch``: torch-CPU restatements of K2-K6 (fp32 sum of squares in
+  double, fp16 copy, widen-add-narrow accumulate, fp32 -> fp16 cast, state
+  birth).
 
 Thread counts are reported with every CPU row.
 
@@ -175,6 +178,36 @@ def cpu_host_k1(n: int, iters: int = 2, threads: int = 0) -> dict:
             "threads": int(N.load().cs_host_threads(threads))}
 
 
+def cpu_torch_chunk_ops(n: int, iters: int = 2) -> List[dict]:
+    """torch-CPU restatements of K2-K6 on host buffers, all threads (SURVEY
+    §8d CPU baseline item 3: the cast and copy of pack / cast)."""
+    g = torch.Generator().manual_seed(0)
+    src16 = (torch.randn(n, generator=g)).half()
+    src32 = torch.randn(n, generator=g)
+    dst16 = torch.zeros(n, dtype=torch.float16)
+    p32, m, v = torch.empty(n), torch.empty(n), torch.empty(n)
+    ops = {
+        "sumsq": lambda: src16.float().square().sum(dtype=torch.float64),
+        "pack": lambda: dst16.copy_(src16),
+        "accumulate": lambda: dst16.copy_(dst16.float().add_(src16.float())),
+        "cast_pack": lambda: dst16.copy_(src32),
+        "master_init": lambda: (p32.copy_(src16), m.zero_(), v.zero_()),
+    }
+    rows = []
+    for name, fn in ops.items():
+        times = []
+        for k in range(iters + 1):
+            t0 = time.perf_counter()
+            fn()
+            if k:
+                times.append(time.perf_counter() - t0)
+        s = min(times)
+        rows.append({"arm": "cpu_torch", "kernel": name, "n": n, "ms": round(s * 1e3, 3),
+                     "gbs": round(BYTES_PER_ELEM[name] * n / s / 1e9, 2),
+                     "threads": torch.get_num_threads()})
+    return rows
+
+
 def run_cpu(sizes_log2: List[int]) -> List[dict]:
     rows = []
     for lg in sizes_log2:
@@ -182,6 +215,7 @@ def run_cpu(sizes_log2: List[int]) -> List[dict]:
         it = 1 if n >= (1 << 29) else 2
         rows.append(cpu_torch_fused_adam(n, it))
         rows.append(cpu_host_k1(n, it))
+        rows.extend(cpu_torch_chunk_ops(n, it))
     return rows
 
 
