@@ -158,6 +158,50 @@ def host_link_peak(dev, nbytes=1 << 30, iters=5):
     return out
 
 
+def host_link_beside_host_adam(dev, threads, chunk=64 << 20, copies=16):
+    """The same pinned copies (fp16 chunk-sized, 128 MiB, rotating over four
+    buffers as the executor's drains and adam_copy do) while the host Adam
+    (cs_adam_chunks_host, the executor's worker team) streams host DRAM:
+    the link ceiling the offloaded step's moves can reach on this host."""
+    import threading
+    import torch
+    from paper_2108_05818_b200 import _native as N
+    from paper_2108_05818_b200 import kernels as K
+    host = [torch.empty(chunk, dtype=torch.float16, pin_memory=True) for _ in range(4)]
+    devb = [torch.empty(chunk, dtype=torch.float16, device=dev) for _ in range(4)]
+    items = [(torch.empty(chunk, dtype=torch.float16).fill_(1e-3), torch.full((chunk,), 0.02),
+              torch.zeros(chunk), torch.zeros(chunk), chunk) for _ in range(4)]
+    st = K.speculate_step_scalars(N.CsStepState(beta1_pow=1.0, beta2_pow=1.0, step=0,
+                                                loss_scale=1.0), K.AdamHyper(lr=1e-4))
+    stop, started = threading.Event(), threading.Event()
+
+    def adam_loop():
+        while not stop.is_set():
+            K.adam_chunks_host(items, K.AdamHyper(lr=1e-4), st, threads)
+            started.set()
+
+    th = threading.Thread(target=adam_loop)
+    th.start()
+    started.wait()
+    out = {}
+    try:
+        for name in ("h2d", "d2h"):
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for i in range(copies):
+                if name == "h2d":
+                    devb[i % 4].copy_(host[i % 4], non_blocking=True)
+                else:
+                    host[i % 4].copy_(devb[i % 4], non_blocking=True)
+            b_.record()
+            torch.cuda.synchronize()
+            out[name] = chunk * 2 * copies / (a.elapsed_time(b_) * 1e-3) / 1e9
+    finally:
+        stop.set()
+        th.join()
+    return out
+
+
 def offload_probe(schema_kw, dev, steps=4, warmup=6):
     """The same 1B step with every optimizer triplet in pinned host DRAM
     (os_placement=cpu): grads D2H + host fused Adam + params H2D as
@@ -208,6 +252,13 @@ def offload_probe(schema_kw, dev, steps=4, warmup=6):
         gbs = nbytes / (t * 1e-3) / 1e9 if t > 0 else None
         moves[key] = {"copies": n, "bytes": nbytes, "achieved_gbs": round(gbs, 1),
                       "peak_gbs": round(peak[key], 1), "frac": round(gbs / peak[key], 3)}
+    try:  # after the trainer's timed steps: the host is otherwise idle
+        beside = host_link_beside_host_adam(dev, tr.executor.worker_threads)
+        for key, m in moves.items():
+            m["ceiling_beside_host_adam_gbs"] = round(beside[key], 1)
+            m["frac_of_that_ceiling"] = round(m["achieved_gbs"] / beside[key], 3)
+    except Exception as e:  # reported, never fatal
+        moves["ceiling_error"] = repr(e)[:200]
     rep = tr.reports[-1]
     out = {"workload": "GPT-1B step, os_placement=cpu (every optimizer triplet in pinned host "
                        "DRAM), B=%d" % schema.batch,
@@ -227,7 +278,7 @@ def offload_probe(schema_kw, dev, steps=4, warmup=6):
            "early_drains": st.early_drains,
            "pinned_host_allocs_during_timing": pinned_allocs,
            "worker_threads": tr.executor.worker_threads, "host_threads": tr.host_threads,
-           "peak_source": "pinned cudaMemcpyAsync 1 GiB"}
+           "peak_source": "pinned cudaMemcpyAsync 1 GiB, host idle; ceiling_beside_host_adam: 128 MiB copies while the host Adam (worker team) streams host DRAM"}
     del tr
     torch.cuda.empty_cache()
     return out
