@@ -58,3 +58,63 @@ def test_eviction_run_recycles_chunk_slabs():
     every_chunk = sum(ch.bytes for ch in cs.chunks.values()) if isinstance(cs.chunks, dict) \
         else sum(ch.bytes for ch in cs.chunks)
     assert pool.slab_bytes < every_chunk
+
+
+def test_side_events_order_only_the_slabs_own_copies():
+    """give(side_events=...): the next taker waits for the slab's own copy on
+    a side stream (its bytes are read before they are overwritten) but not
+    for unrelated work queued behind it on that stream."""
+    from paper_2108_05818_b200.slabs import SlabPool
+    compute, d2h = torch.cuda.current_stream(), torch.cuda.Stream()
+    pool = SlabPool(torch.device("cuda", 0), [compute, d2h], max_free=4)
+    n = 1 << 24
+    a = pool.take(n, torch.float16, compute)
+    a.fill_(3.0)
+    host = torch.empty(n, dtype=torch.float16, pin_memory=True)
+    d2h.wait_stream(compute)
+    with torch.cuda.stream(d2h):
+        torch.cuda._sleep(20_000_000)            # the copy lands late ...
+        host.copy_(a, non_blocking=True)
+        own = torch.cuda.Event()
+        own.record(d2h)
+        torch.cuda._sleep(400_000_000)           # ... and unrelated work queues behind it
+    assert pool.give(a, [own])
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(compute)
+    b = pool.take(n, torch.float16, compute)
+    assert b.data_ptr() == a.data_ptr()
+    b.fill_(7.0)                                  # must not reach the copy's source early
+    t1.record(compute)
+    t1.synchronize()
+    assert bool((host == 3.0).all())              # the copy read the slab before the refill
+    slept = t0.elapsed_time(t1)
+    # the taker waited for the late copy (~20M cycles) but not for the 400M-cycle tail
+    ev_tail = torch.cuda.Event(enable_timing=True)
+    ev_tail.record(d2h)
+    ev_tail.synchronize()
+    assert slept < 0.5 * t0.elapsed_time(ev_tail), (slept, t0.elapsed_time(ev_tail))
+
+
+def test_side_events_free_to_the_allocator_in_compute_order():
+    """Beyond max_free a slab goes back to the caching allocator; with side
+    events the compute stream waits for them first, so a later allocation
+    on the compute stream cannot overwrite bytes a copy still reads."""
+    from paper_2108_05818_b200.slabs import SlabPool
+    compute, d2h = torch.cuda.current_stream(), torch.cuda.Stream()
+    pool = SlabPool(torch.device("cuda", 0), [compute, d2h], max_free=0)
+    n = 1 << 24
+    a = pool.take(n, torch.float16, compute)
+    a.fill_(5.0)
+    host = torch.empty(n, dtype=torch.float16, pin_memory=True)
+    d2h.wait_stream(compute)
+    with torch.cuda.stream(d2h):
+        torch.cuda._sleep(50_000_000)
+        host.copy_(a, non_blocking=True)
+        own = torch.cuda.Event()
+        own.record(d2h)
+    assert pool.give(a, [own])
+    del a
+    c = torch.empty(n, dtype=torch.float16, device="cuda")  # may reuse the block
+    c.fill_(9.0)
+    torch.cuda.synchronize()
+    assert bool((host == 5.0).all())
