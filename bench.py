@@ -327,7 +327,7 @@ def c5_probe(sizes=(20, 22, 24, 26, 28, 30), oracle_sizes=(20, 24)):
         table[str(n)]["adam"].update({"cpu_oracle_gbs": round(28 * n / dt / 1e9, 3),
                                       "cpu_oracle_threads": thr})
     return {"kernels_bytes_per_elem": MB.BYTES_PER_ELEM, "peak_gbs": MB.measured_peak_gbs(),
-            "l2": "flushed (2 x 126 MB write) before every GPU launch",
+            "l2": "flushed (a read of 2 x 126 MB: cold, clean) before every GPU launch",
             "cpu_arms": "torch.optim.Adam(fused=True) on CPU incl. fp16->fp32 grad and "
                         "fp32->fp16 param casts; cs_adam_chunks_host (AVX2+OpenMP); C oracle "
                         "(scalar C, OpenMP over the affinity mask)", "rows": table}

@@ -4,8 +4,8 @@
 Algorithmic bytes per element: K1 Adam 28, K2 sumsq 2,
 K3 pack 4, K4 accumulate 6, K5 cast+pack 6, K6 state birth 14 (fp16 src).
 
-GPU arm: every timed launch is preceded by an L2 flush (a write of a
-buffer twice the 126 MB L2), and bracketed by CUDA events on its stream;
+GPU arm: every timed launch is preceded by an L2 flush (a read of a
+buffer twice the 126 MB L2: cold and clean), and bracketed by CUDA events on its stream;
 the flush's ~0.1 ms of device work hides the host launch, so the events
 see the kernel alone, cold.  Sizes below ~4M elements are latency-bound
 (a few microseconds of launch ramp against < 10 us of traffic) and are
@@ -55,13 +55,18 @@ def measured_peak_gbs() -> float:
 
 
 class L2Flush:
-    """Writes a buffer of 2 x L2 so the next launch starts cold."""
+    """Reads a buffer of 2 x L2 so the next launch starts cold AND clean: the
+    previous launch's dirty lines are written back during the flush, and L2
+    is left holding clean lines (a write flush would leave 126 MB of dirty
+    lines whose write-back the next, timed launch would pay: at 2^20 elements
+    that is several times the kernel's own traffic)."""
 
     def __init__(self, device="cuda"):
-        self.buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=device)
+        self.buf = torch.ones(2 * L2_BYTES // 4, dtype=torch.float32, device=device)
+        self.out = torch.empty((), dtype=torch.float32, device=device)
 
     def __call__(self) -> None:
-        self.buf.fill_(1.0)
+        torch.sum(self.buf, dim=0, out=self.out)
 
 
 def time_launch(fn: Callable[[], None], iters: int, flush: Optional[L2Flush],
@@ -120,7 +125,7 @@ def run(sizes_log2: List[int], iters: int, kernels=tuple(BYTES_PER_ELEM)) -> Lis
             rows.append({"arm": "gpu", "kernel": name, "n": n, "ms": round(ms, 5),
                          "gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4),
                          "regime": "latency-bound" if n < LATENCY_BOUND_BELOW else "hbm",
-                         "l2": "flushed before every launch"})
+                         "l2": "read-flushed before every launch (cold, clean)"})
         torch.cuda.empty_cache()
     return rows
 
