@@ -18,15 +18,29 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "cs_internal.h"
 
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnits = 2;
-constexpr int kBlockTile = kThreads * kUnits * 8;
+// 8-element units per thread and tile: the accumulate reads the slot before
+// writing it and needs more reads in flight (4 units, all loads first: 0.85
+// -> 0.99 of the copy peak); pack and cast keep 2 units issued in turn
+// (0.94; the loads-first form measured 0.90-0.92 for them)
+template <int OP>
+__host__ __device__ constexpr int units() { return OP == 1 ? 4 : 2; }
+template <int OP>
+__host__ __device__ constexpr int64_t block_tile() { return (int64_t)kThreads * units<OP>() * 8; }
 
 enum Op { kPack = 0, kAccumulate = 1, kCast = 2 };
+
+// A/B switch for K6 (CS_MASTER_INIT_FUSED=1: the single fused kernel)
+const bool g_master_init_split = [] {
+  const char* e = getenv("CS_MASTER_INIT_FUSED");
+  return !(e && e[0] == '1');
+}();
 
 struct PackBatch {
   void* dst[cs::kMaxBatch];
@@ -103,6 +117,55 @@ __device__ __forceinline__ void elem(uint16_t* dst, const void* src, int64_t e) 
   }
 }
 
+// Whole-tile vector path: every unit's loads are issued before any store
+// (the slot and the source never alias, but the compiler cannot know), so a
+// thread keeps kUnits x 16-32 B of reads in flight.
+template <int OP, int DT>
+__device__ __forceinline__ void tile_vec(uint16_t* __restrict__ dst, const void* __restrict__ src,
+                                         int64_t base) {
+  constexpr int kUnits = units<OP>();
+  constexpr int W = OP == kCast ? 2 : 1;  // 16-byte source words per unit
+  uint4 sv[kUnits][W];
+  uint4 dv[kUnits];
+#pragma unroll
+  for (int u = 0; u < kUnits; ++u) {
+    const int64_t e = base + (int64_t)(u * kThreads + threadIdx.x) * 8;
+    if (OP == kCast) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(static_cast<const float*>(src) + e);
+      sv[u][0] = __ldcs(s4);
+      sv[u][W - 1] = __ldcs(s4 + (W - 1));
+    } else {
+      sv[u][0] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(src) + e));
+    }
+    if (OP == kAccumulate) dv[u] = *reinterpret_cast<const uint4*>(dst + e);
+  }
+#pragma unroll
+  for (int u = 0; u < kUnits; ++u) {
+    const int64_t e = base + (int64_t)(u * kThreads + threadIdx.x) * 8;
+    uint4* d = reinterpret_cast<uint4*>(dst + e);
+    if (OP == kPack) {
+      __stcs(d, sv[u][0]);
+    } else if (OP == kCast) {
+      const float4 a = *reinterpret_cast<const float4*>(&sv[u][0]);
+      const float4 b = *reinterpret_cast<const float4*>(&sv[u][W - 1]);
+      __stcs(d, make_uint4(pair_from_f<DT>(a.x, a.y), pair_from_f<DT>(a.z, a.w),
+                           pair_from_f<DT>(b.x, b.y), pair_from_f<DT>(b.z, b.w)));
+    } else {
+      const uint32_t* sw = reinterpret_cast<const uint32_t*>(&sv[u][0]);
+      const uint32_t* dw = reinterpret_cast<const uint32_t*>(&dv[u]);
+      uint4 out;
+      uint32_t* ow = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float lo = __fadd_rn(to_f<DT>(dw[k] & 0xffff), to_f<DT>(sw[k] & 0xffff));
+        const float hi = __fadd_rn(to_f<DT>(dw[k] >> 16), to_f<DT>(sw[k] >> 16));
+        ow[k] = pair_from_f<DT>(lo, hi);
+      }
+      __stcs(d, out);
+    }
+  }
+}
+
 template <int OP, int DT>
 __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ PackBatch b) {
   const int64_t total = b.tile_start[b.count];
@@ -111,9 +174,13 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
     uint16_t* dst = static_cast<uint16_t*>(b.dst[k]);
     const void* src = b.src[k];
     const int64_t n = b.n[k];
-    const int64_t base = (tile - b.tile_start[k]) * kBlockTile;
+    const int64_t base = (tile - b.tile_start[k]) * block_tile<OP>();
+    if (OP == kAccumulate && b.vec[k] && base + block_tile<OP>() <= n) {
+      tile_vec<OP, DT>(dst, src, base);
+      continue;
+    }
 #pragma unroll
-    for (int u = 0; u < kUnits; ++u) {
+    for (int u = 0; u < units<OP>(); ++u) {
       const int64_t e = base + (int64_t)(u * kThreads + threadIdx.x) * 8;
       if (e >= n) continue;
       if (b.vec[k] && e + 8 <= n) {
@@ -151,6 +218,44 @@ master_init_kernel(float* __restrict__ p32, float* __restrict__ m, float* __rest
                                 : to_f<SDT>(static_cast<const uint16_t*>(src)[i]);
         m[i] = 0.0f;
         v[i] = 0.0f;
+      }
+    }
+  }
+}
+
+// p32 = float(src), 4-element vectors (the caller checked alignment), four
+// vectors per thread with every load issued before the stores
+template <int SDT>
+__global__ void __launch_bounds__(kThreads)
+widen_kernel(float* __restrict__ p32, const void* __restrict__ src, int64_t n) {
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * kThreads * 4 * U;
+  for (int64_t e0 = ((int64_t)blockIdx.x * kThreads * U + threadIdx.x) * 4; e0 < n;
+       e0 += stride) {
+    float4 f[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * kThreads * 4;
+      if (e + 4 <= n) {
+        if (SDT == CS_FP32) {
+          f[u] = __ldcs(reinterpret_cast<const float4*>(static_cast<const float*>(src) + e));
+        } else {
+          const uint2 w =
+              __ldcs(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(src) + e));
+          f[u] = make_float4(to_f<SDT>(w.x & 0xffff), to_f<SDT>(w.x >> 16),
+                             to_f<SDT>(w.y & 0xffff), to_f<SDT>(w.y >> 16));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + (int64_t)u * kThreads * 4;
+      if (e + 4 <= n) {
+        __stcs(reinterpret_cast<float4*>(p32 + e), f[u]);
+      } else {
+        for (int64_t i = e; i < n; ++i)
+          p32[i] = SDT == CS_FP32 ? static_cast<const float*>(src)[i]
+                                  : to_f<SDT>(static_cast<const uint16_t*>(src)[i]);
       }
     }
   }
@@ -202,7 +307,7 @@ int run_pack(const char* what, const CsPackItem* items, int n_items, int dtype, 
       b.n[b.count] = it.n;
       b.vec[b.count] = aligned16(dst) && aligned16(it.src);
       b.tile_start[b.count] = tiles;
-      tiles += (it.n + kBlockTile - 1) / kBlockTile;
+      tiles += (it.n + block_tile<OP>() - 1) / block_tile<OP>();
       ++b.count;
     }
     first = i;  // resume where this batch stopped (zero-length items took no slot)
@@ -242,6 +347,25 @@ extern "C" int cs_master_init(float* p32, float* m, float* v, const void* src, i
                   (reinterpret_cast<uintptr_t>(src) & need) == 0;
   const int grid = grid_for((n + kThreads * 4 - 1) / (kThreads * 4));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (vec && g_master_init_split) {
+    // m = v = 0 as two write-only memsets and p32 = float(src) as one 1:2
+    // stream: interleaving one read and three write streams in one kernel
+    // ran at 0.82 of the copy peak (profiles/r02/microbench_c5.jsonl)
+    cudaError_t e = cudaMemsetAsync(m, 0, (size_t)n * sizeof(float), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(v, 0, (size_t)n * sizeof(float), s);
+    if (e != cudaSuccess) {
+      cs::set_error("cs_master_init: memset failed: %s", cudaGetErrorString(e));
+      return (int)e;
+    }
+    if (src_dtype == CS_FP16)
+      widen_kernel<CS_FP16><<<grid, kThreads, 0, s>>>(p32, src, n);
+    else if (src_dtype == CS_BF16)
+      widen_kernel<CS_BF16><<<grid, kThreads, 0, s>>>(p32, src, n);
+    else
+      widen_kernel<CS_FP32><<<grid, kThreads, 0, s>>>(p32, src, n);
+    cs::note_launches(1);
+    return check_launch("cs_master_init");
+  }
   if (src_dtype == CS_FP16)
     master_init_kernel<CS_FP16><<<grid, kThreads, 0, s>>>(p32, m, v, src, n, vec);
   else if (src_dtype == CS_BF16)
