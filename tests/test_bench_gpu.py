@@ -38,6 +38,22 @@ def test_bench_single_gpu_line():
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["achieved"] > 0
 
 
+def test_bench_offload_probe_fields():
+    """The side measurement with every optimizer triplet in host DRAM: chunk
+    moves against the idle pinned peak and against the ceiling measured
+    beside the host Adam in the same run."""
+    args = [a for a in SMALL if a != "--no-offload-probe"]
+    res = subprocess.run([sys.executable, "bench.py", *args], cwd=ROOT, capture_output=True,
+                         text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    probe = _line(res.stdout)["offload_probe"]
+    assert probe["ms_per_step"] > 0 and probe["host_adam_gelem_per_s"] > 0
+    for key in ("d2h", "h2d"):
+        m = probe["chunk_moves"][key]
+        assert m["copies"] > 0 and m["achieved_gbs"] > 0 and 0 < m["frac"]
+        assert m["ceiling_beside_host_adam_gbs"] > 0 and m["frac_of_that_ceiling"] > 0
+
+
 def test_bench_two_ranks_gloo_same_device():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + os.getpid() % 200),
