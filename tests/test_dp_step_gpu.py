@@ -44,7 +44,13 @@ def _batches(schema, rank, n):
             for _ in range(n)]
 
 
+def _split(place):
+    """"gpu_host": the GPU operator with its weights and state in host DRAM."""
+    return ("gpu", "host") if place == "gpu_host" else (place, "hbm")
+
+
 def _worker(rank, world, port, outdir, case, place="plan", async_adam=False):
+    place, emb_weights = _split(place)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -57,7 +63,7 @@ def _worker(rank, world, port, outdir, case, place="plan", async_adam=False):
         tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
                           dtype=torch.float16, seed=0, embedding_placement=place,
                           untied_head=True if place != "plan" else None,
-                          async_host_adam=async_adam)
+                          async_host_adam=async_adam, embedding_weights=emb_weights)
         assert tr.nproc == world and tr.rank == rank
         losses = [tr.step_host(b) for b in _batches(schema, rank, ITERS)]
         reports = [{"transfers": [[t.moment, t.chunk_id, t.src, t.dst, t.bytes, t.reason]
@@ -78,10 +84,12 @@ def _worker(rank, world, port, outdir, case, place="plan", async_adam=False):
     ("tiny_p2", 2, "plan", False), ("tiny_p4_tight", 4, "plan", False),
     ("tiny_p8", 8, "plan", False), ("tiny_p2_ckpt", 2, "plan", False),
     ("tiny_p2", 2, "gpu", False),          # device embedding operator, grads all-reduced
-    ("tiny_p4_tight", 4, "cpu", True)])    # host embedding + async host Adam under ZeRO
+    ("tiny_p4_tight", 4, "cpu", True),     # host embedding + async host Adam under ZeRO
+    ("tiny_p2", 2, "gpu_host", False)])    # device operator, weights + state on the host
 def test_multi_rank_zero_step_on_one_gpu(case, world, place, async_adam):
     with tempfile.TemporaryDirectory() as d:
-        port = 29800 + world * 10 + (place == "gpu") + 2 * async_adam + os.getpid() % 50 * 40
+        port = (29800 + world * 10 + (place == "gpu") + 2 * async_adam + 4 * (place == "gpu_host")
+                + os.getpid() % 50 * 40)
         mp.spawn(_worker, args=(world, port, d, case, place, async_adam),
                  nprocs=world, join=True)
         res = [torch.load(os.path.join(d, "rank%d.pt" % r), weights_only=False)
@@ -104,9 +112,11 @@ def test_multi_rank_zero_step_on_one_gpu(case, world, place, async_adam):
     kw["batch"] = kw["batch"] * world
     schema2 = build_gpt_schema(**kw)
     schema1 = build_gpt_schema(**c["schema"])
+    place1, emb_weights = _split(place)
     tr = ChunkTrainer(schema2, PolicySpec(**c["policy"]), HardwareSpec(gpu_count=1,
                       gpu_bytes=180 * 10**9), dtype=torch.float16, seed=0,
-                      embedding_placement=place, untied_head=True if place != "plan" else None)
+                      embedding_placement=place1, untied_head=True if place != "plan" else None,
+                      embedding_weights=emb_weights)
     per_rank = [_batches(schema1, r, ITERS) for r in range(world)]
     single = [tr.step_host(torch.cat([per_rank[r][i] for r in range(world)]))
               for i in range(ITERS)]
