@@ -109,20 +109,24 @@ def plan_early_fetches(fetches, used, capacity: int, margin: int, adam_index: in
     (moment, GPU pool bytes in use) of the last iteration's samples (the grid
     puts moment 2e before event e and 2e+1 during it, `model.py:209-214`).
     Fetch j, with cumulative bytes B_j, goes before the earliest event e whose
-    usage from moment 2e up to ADAM stayed at most capacity - margin - B_j:
-    holding every earlier-issued fetch as well, nothing the last iteration
-    used before ADAM would have been short of room.  Fetches that would land
-    after ``last_event`` (and every one after them: the walk's order is kept)
-    are left to the ordinary prefetch."""
+    usage from moment 2e up to the moment before ADAM (2 * adam_index) stayed
+    at most capacity - margin - B_j: holding every earlier-issued fetch as
+    well, nothing the last iteration used before ADAM would have been short
+    of room.  ADAM's own moment is not counted: its usage already includes
+    these fetches, and since the early ones are a prefix of the walk's
+    fetches, the walk adopts all of them before it fetches anything else.
+    Fetches that would land after ``last_event`` (and every one after them:
+    the walk's order is kept) are left to the ordinary prefetch."""
     peak: Dict[int, int] = {}
     for m, b in used:
         peak[m] = max(peak.get(m, 0), b)
     if not peak or not fetches:
         return {}
     first = min(peak) // 2
-    head: Dict[int, int] = {}  # capacity - margin - max usage over [2e, 2*adam_index + 1]
-    run = 0
-    for e in range(adam_index, first - 1, -1):
+    head: Dict[int, int] = {}  # capacity - margin - max usage over [2e, 2*adam_index]
+    run = peak.get(2 * adam_index, 0)
+    head[adam_index] = capacity - margin - run
+    for e in range(adam_index - 1, first - 1, -1):
         run = max(run, peak.get(2 * e, 0), peak.get(2 * e + 1, 0))
         head[e] = capacity - margin - run
     out: Dict[int, List[int]] = {}

@@ -34,6 +34,7 @@ from test_fuzz_step_gpu import _config, _rows, _tight_budget  # noqa: E402
 
 ITERS = 6
 SEEDS = [1, 4, 6, 9, 13, 16, 20]  # configurations whose ledger evicts chunks
+EARLY = {1, 6, 16, 20}  # ... and whose backward leaves room for early ADAM fetches
 
 
 def _run(seed, mispredict=False):
@@ -97,6 +98,8 @@ def _run(seed, mispredict=False):
         and tr.sim.chunk_set.chunks[t.chunk_id].list_kind is not ChunkKind.PARAM_FP16
         and t.moment < 2 * tr._events[-1].index + 1
         for t in tr.reports[-1].transfers if isinstance(t.chunk_id, int))
+    print("seed %d: preevict hits %d, early ADAM fetches %d" % (
+        seed, st.preevict_hits, st.adam_prefetch_early))
     return st, os_evicted_before_adam
 
 
@@ -106,9 +109,49 @@ def test_preevict_and_early_adam_fetch(seed):
     if os_evicted:
         assert st.preevict_hits > 0, seed
         assert st.preevict_discarded == 0, seed  # the schedule is at its fixed point
+    if seed in EARLY:
+        assert st.adam_prefetch_early > 0 and st.adam_prefetch_oom == 0, seed
 
 
 @pytest.mark.parametrize("seed", [1, 6, 16])
 def test_mispredicted_preevictions_are_discarded(seed):
     st, _ = _run(seed, mispredict=True)
     assert st.preevict_discarded > 0, seed
+
+
+def test_long_offload_run_holds_memory_constant():
+    """15 iterations of a tight-budget configuration with pre-evictions and
+    early ADAM fetches (seed 6's generator, chunk moves landing late): HBM
+    allocated, pinned host bytes held by the executor and the slab pool stop
+    growing once the schedule is at its fixed point, and nothing is ever
+    discarded (the prediction holds every iteration)."""
+    from paper_2108_05818_b200 import kernels as K
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    schema_kw, policy, dtype, slack, knobs, hyper = _config(6)
+    budget = _tight_budget(schema_kw, policy, slack)
+    schema = build_gpt_schema(**schema_kw)
+    tr = ChunkTrainer(schema, PolicySpec(**policy), HardwareSpec(gpu_count=1, gpu_bytes=budget),
+                      dtype=dtype, seed=0, untied_head=True, hyper=K.AdamHyper(**hyper), **knobs)
+    tr.executor.copy_delay_cycles = 200_000
+    g = torch.Generator().manual_seed(6)
+    marks = []
+    for i in range(15):
+        tr.step_host(torch.randint(0, schema.vocab, (schema.batch, schema.seq_len + 1),
+                                   generator=g))
+        tr.finish_host_work()
+        torch.cuda.synchronize()
+        ex = tr.executor
+        pinned = sum(t.numel() * t.element_size() for t in ex.payload["cpu"].values()) + \
+            ex._free_host_bytes
+        marks.append((torch.cuda.memory_allocated(), pinned, ex.slabs.slab_bytes,
+                      len(ex._preevicted), len(ex._side_use)))
+    st = tr.executor.stats
+    assert st.preevict_hits > 0 and st.preevict_discarded == 0
+    assert st.adam_prefetch_oom == 0
+    assert st.adam_prefetch_early > 0
+    print("early ADAM fetches", st.adam_prefetch_early, "pre-evictions", st.preevict_hits)
+    steady = marks[5:]
+    assert len({m[0] for m in steady}) == 1, marks      # HBM allocated
+    assert len({m[1] for m in steady}) == 1, marks      # pinned payloads + free list
+    assert len({m[2] for m in steady}) == 1, marks      # slab pool high-water mark
+    assert max(m[4] for m in steady) <= max(m[4] for m in marks[:5]) + 8, marks

@@ -1,7 +1,8 @@
 """``plan_early_fetches``: where ADAM's fetches are issued ahead of the ledger
 (host logic of the payload executor; no GPU).  Properties: every placed fetch
 fits, together with every fetch placed at or before its event, under the
-capacity minus the margin at every later moment up to ADAM; placement is as
+capacity minus the margin at every later moment up to the one before ADAM
+(ADAM's own usage already counts them); placement is as
 early as that allows; the walk's order is kept; nothing lands after the last
 event."""
 
@@ -21,13 +22,13 @@ def _check(fetches, used, cap, margin, adam, last, out):
     for e, cid in placed:
         assert e <= last
         held = sum(size[c] for f, c in placed if f <= e or order.index(c) <= order.index(cid))
-        for m in range(2 * e, 2 * adam + 2):
+        for m in range(2 * e, 2 * adam + 1):  # up to the moment before ADAM
             assert peak.get(m, 0) + held <= cap - margin, (e, cid, m)
         # not placeable one event earlier
         if e > min(peak) // 2:
             held_before = sum(size[c] for c in order[:order.index(cid) + 1])
             assert any(peak.get(m, 0) + held_before > cap - margin
-                       for m in range(2 * (e - 1), 2 * adam + 2))
+                       for m in range(2 * (e - 1), 2 * adam + 1))
 
 
 def test_known_answer():
