@@ -141,15 +141,19 @@ int cs_adam_variant(int v);
 
 /* ---- K2: gradient sum of squares -------------------------------------------
  * Global grad-norm / found-inf for clipping and dynamic loss scaling (no
- * reference counterpart: the simulator has no numerics).  Writes one fp32
- * partial per block into d_partials[0..n_partials) (n_partials must equal
- * cs_sumsq_partials()); cs_sumsq_finalize reduces them in a fixed order
- * (deterministic) into d_state->sumsq (accumulate=1 adds to it). */
-int cs_sumsq_partials(void);
-int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
-                  float* d_partials, void* stream);
-int cs_sumsq_finalize(const float* d_partials, int n_partials,
-                      CsStepState* d_state, int accumulate, void* stream);
+ * reference counterpart: the simulator has no numerics), in a canonical order
+ * that does not depend on placement (HBM or host DRAM) or batching: each item
+ * gets a double S_i defined tile by tile (specification in sumsq.cu, restated
+ * by the C oracle); cs_grad_sumsq writes S_i into d_item_sums[slots[i]]
+ * (slots NULL: i), cs_grad_sumsq_host computes the same S_i for items in host
+ * memory, and cs_sumsq_finalize folds d_item_sums[0..n_slots) in slot order
+ * (double) into d_state->sumsq.  d_scratch holds cs_sumsq_scratch(items)
+ * floats (1/1024 of the gradient bytes). */
+int64_t cs_sumsq_scratch(const CsGradItem* items, int n_items);
+int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype, const int* slots,
+                  float* d_scratch, int64_t scratch_elems, double* d_item_sums, void* stream);
+int cs_sumsq_finalize(const double* d_item_sums, int n_slots, CsStepState* d_state,
+                      void* stream);
 
 /* ---- step scalars -------------------------------------------------------------
  * Device-side: consume d_state->sumsq, decide skip, clip coefficient,
@@ -201,9 +205,10 @@ int cs_adam_chunks_host(const CsAdamItem* items, int n_items, int dtype,
 int cs_adam_chunks_host_oop(const CsAdamItem* in, const CsAdamItem* out, int n_items, int dtype,
                             const CsAdamHyper* hyper, const CsStepState* state, int n_threads);
 
-/* Host sum of squares (double accumulation) of fp16/bf16 gradients that sit
- * in host DRAM (grads of a chunk evicted to the CPU before the ADAM event,
- * or of CPU-placed positions); contributes to CsStepState.sumsq. */
+/* Host twin of K2 for gradients in host DRAM (a chunk evicted to the CPU
+ * before the ADAM event, CPU-placed positions, the CPU-placed embedding):
+ * out[i] = S_i of items[i], bit-identical to what cs_grad_sumsq would write
+ * for the same bytes in HBM. */
 int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtype, double* out,
                        int n_threads);
 

@@ -35,6 +35,7 @@
  * narrowing by round-to-nearest-even implemented here in integer code.
  */
 #include <math.h>
+#include <stdlib.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -192,6 +193,67 @@ double or_grad_sumsq(const uint16_t* g, int64_t n, int dtype) {
     acc += f * f;
   }
   return acc;
+}
+
+/* ---- K2's canonical order (paper_2108_05818_b200/csrc/sumsq.cu) ----------
+ * S(item): zero-padded 8192-element tiles; lane tau, group u, j: element
+ * 8192 t + (256 u + tau) 8 + j; a_j folds x*x over u (fp32); the lane value
+ * is the fixed fp32 tree over a_0..a_7; each warp of 32 lanes is an
+ * xor-butterfly (o = 16..1) of fp32 adds; the (tile, warp) partials are
+ * summed in double by 8192 strided folds, 32 fixed trees of 256 and an
+ * ordered fold of the 32 group values.  Scalar C, every
+ * fp32 operation rounded on its own (-ffp-contract=off). */
+
+double or_grad_sumsq_item(const uint16_t* g, int64_t n, int dtype) {
+  const int64_t tiles = (n + 8191) / 8192;
+  const int64_t q_n = tiles * 8;
+  float* part = (float*)malloc((size_t)(q_n > 0 ? q_n : 1) * sizeof(float));
+  for (int64_t t = 0; t < tiles; ++t) {
+    float lane[256];
+    for (int tau = 0; tau < 256; ++tau) {
+      float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int u = 0; u < 4; ++u)
+        for (int j = 0; j < 8; ++j) {
+          const int64_t e = 8192 * t + (256 * (int64_t)u + tau) * 8 + j;
+          const float x = e < n ? (float)widen(g[e], dtype) : 0.0f;
+          const float sq = x * x;
+          a[j] = a[j] + sq;
+        }
+      const float l01 = a[0] + a[1], l23 = a[2] + a[3], l45 = a[4] + a[5], l67 = a[6] + a[7];
+      const float lo = l01 + l23, hi = l45 + l67;
+      lane[tau] = lo + hi;
+    }
+    for (int w = 0; w < 8; ++w) {
+      float v[32], nv[32];
+      for (int l = 0; l < 32; ++l) v[l] = lane[32 * w + l];
+      for (int o = 16; o > 0; o >>= 1) {
+        for (int l = 0; l < 32; ++l) nv[l] = v[l] + v[l ^ o];
+        for (int l = 0; l < 32; ++l) v[l] = nv[l];
+      }
+      part[8 * t + w] = v[0];
+    }
+  }
+  double total = 0.0;
+  for (int c = 0; c < 32; ++c) {      /* 32 groups of 256 strands, stride 8192 */
+    double d[256];
+    for (int r = 0; r < 256; ++r) {
+      double acc = 0.0;
+      for (int64_t q = 256 * c + r; q < q_n; q += 8192) acc = acc + (double)part[q];
+      d[r] = acc;
+    }
+    for (int w = 128; w > 0; w >>= 1)
+      for (int r = 0; r < w; ++r) d[r] = d[r] + d[r + w];
+    total = total + d[0];
+  }
+  free(part);
+  return total;
+}
+
+/* the global value: the item sums folded in slot order, rounded to fp32 */
+float or_sumsq_total(const double* item_sums, int n) {
+  double t = 0.0;
+  for (int i = 0; i < n; ++i) t = t + item_sums[i];
+  return (float)t;
 }
 
 /* ---- pack / accumulate / cast / optimizer-state birth ------------------- */

@@ -50,6 +50,10 @@ def lib() -> ctypes.CDLL:
             [ctypes.c_int, ctypes.POINTER(OrStepState), ctypes.c_int]
         L.or_grad_sumsq.restype = ctypes.c_double
         L.or_grad_sumsq.argtypes = [P, ctypes.c_int64, ctypes.c_int]
+        L.or_grad_sumsq_item.restype = ctypes.c_double
+        L.or_grad_sumsq_item.argtypes = [P, ctypes.c_int64, ctypes.c_int]
+        L.or_sumsq_total.restype = ctypes.c_float
+        L.or_sumsq_total.argtypes = [P, ctypes.c_int]
         L.or_pack.argtypes = [P, ctypes.c_int64, P, ctypes.c_int64, ctypes.c_int, ctypes.c_int]
         L.or_cast_pack.argtypes = [P, ctypes.c_int64, P, ctypes.c_int64, ctypes.c_int]
         L.or_master_init.argtypes = [P, P, P, P, ctypes.c_int, ctypes.c_int64]
@@ -82,7 +86,18 @@ def adam(p16: np.ndarray, p32: np.ndarray, m: np.ndarray, v: np.ndarray, n: int,
 
 
 def grad_sumsq(g16: np.ndarray, dtype: int) -> float:
+    """Plain double sum of squares (reference value for tolerance checks)."""
     return lib().or_grad_sumsq(_p(g16), g16.size, dtype)
+
+
+def grad_sumsq_item(g16: np.ndarray, dtype: int) -> float:
+    """K2's canonical per-item value S (bit-exact target of K2 and its host twin)."""
+    return lib().or_grad_sumsq_item(_p(g16), g16.size, dtype)
+
+
+def sumsq_total(item_sums) -> float:
+    a = np.ascontiguousarray(np.asarray(item_sums, dtype=np.float64))
+    return lib().or_sumsq_total(_p(a), a.size)
 
 
 def pack(chunk: np.ndarray, offset: int, src: np.ndarray, dtype: int, accumulate: bool) -> None:

@@ -19,7 +19,8 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libchunkstar_b200.so")
 
-CUDA_SOURCES = ["adam.cu", "adam_tma.cu", "pack.cu", "xent.cu", "layernorm.cu", "embed.cu"]
+CUDA_SOURCES = ["adam.cu", "adam_tma.cu", "sumsq.cu", "pack.cu", "xent.cu", "layernorm.cu",
+                "embed.cu"]
 HOST_SOURCES = ["host_adam.cpp", "host_embed.cpp", "capi.cpp", "gemm_gelu.cpp", "comm.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -53,12 +53,13 @@ SIGNATURES = {
     "cs_adam_chunks": (ctypes.c_int, [ctypes.POINTER(CsAdamItem), ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(CsAdamHyper), ctypes.c_void_p,
                                       ctypes.c_void_p]),
-    "cs_sumsq_partials": (ctypes.c_int, []),
+    "cs_sumsq_scratch": (ctypes.c_int64, [ctypes.POINTER(CsGradItem), ctypes.c_int]),
     "cs_adam_variant": (ctypes.c_int, [ctypes.c_int]),
     "cs_grad_sumsq": (ctypes.c_int, [ctypes.POINTER(CsGradItem), ctypes.c_int, ctypes.c_int,
-                                     ctypes.c_void_p, ctypes.c_void_p]),
+                                     ctypes.POINTER(ctypes.c_int), ctypes.c_void_p,
+                                     ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "cs_sumsq_finalize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
-                                         ctypes.c_int, ctypes.c_void_p]),
+                                         ctypes.c_void_p]),
     "cs_step_state_init": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p]),
     "cs_adam_prepare": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(CsAdamHyper),
                                        ctypes.c_float, ctypes.c_float, ctypes.c_float,

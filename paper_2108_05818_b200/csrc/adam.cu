@@ -1,5 +1,5 @@
-// K1 fused chunk Adam, K2 gradient sum-of-squares and the device-side step
-// scalars for the chunk-managed training step on B200 (sm_100a).
+// K1 fused chunk Adam and the device-side step scalars for the chunk-managed
+// training step on B200 (sm_100a); K2 (sum of squares) is in sumsq.cu.
 //
 // K1 realises Engine._adam_event's per-position update
 // (/root/reference/pkg/src/chunkstar/engine.py:225-272): it reads the fp16
@@ -31,8 +31,6 @@
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kGroups = 4;   // 4-element groups per thread per block tile (K2)
-constexpr int kSumsqTile = kThreads * kGroups * 8;  // K2: 128-bit groups
 // K1 data-movement variants, bit-identical results.  Selected once per
 // process (CS_ADAM_VARIANT, default kAdamDefault):
 //   0  SIMT register-tiled (this file; also the fallback for items whose
@@ -49,13 +47,6 @@ struct AdamBatch {
   int n;
   float b2, c1, c2, eps, wd, decay;  // scalars formed in double, rounded once
   int adamw;
-};
-
-struct GradBatch {
-  CsGradItem item[cs::kMaxBatch];
-  int64_t tile_start[cs::kMaxBatch + 1];
-  int n;
-  int accumulate;  // 0: first batch of a call overwrites the partials
 };
 
 // ---- 16-bit storage helpers (4 elements = 64 bits) -------------------------
@@ -216,80 +207,6 @@ adam_chunks_kernel(const __grid_constant__ AdamBatch b, const CsStepState* __res
   }
 }
 
-// ---- K2: sum of squares of fp16/bf16 gradients -----------------------------
-
-__device__ __forceinline__ float block_sum(float x) {
-  __shared__ float warp_sums[kThreads / 32];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) warp_sums[warp] = x;
-  __syncthreads();
-  float s = 0.0f;
-  if (warp == 0) {
-    s = lane < kThreads / 32 ? warp_sums[lane] : 0.0f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  }
-  return s;  // valid in thread 0
-}
-
-template <int DT>
-__global__ void __launch_bounds__(kThreads)
-grad_sumsq_kernel(const __grid_constant__ GradBatch b, float* __restrict__ partials) {
-  float acc = 0.0f;
-  const int64_t total = b.tile_start[b.n];
-  for (int64_t tile = blockIdx.x; tile < total; tile += gridDim.x) {
-    const int k = find_item(b.tile_start, b.n, tile);
-    const CsGradItem it = b.item[k];
-    const int64_t base = (tile - b.tile_start[k]) * kSumsqTile;
-    const uint16_t* __restrict__ g16 = static_cast<const uint16_t*>(it.g16);
-    if (base + kSumsqTile <= it.n && (reinterpret_cast<uintptr_t>(g16) & 15) == 0) {
-      // four 128-bit loads in flight per thread before any math
-      uint4 g[kGroups];
-#pragma unroll
-      for (int u = 0; u < kGroups; ++u)
-        g[u] = __ldcs(reinterpret_cast<const uint4*>(
-            g16 + base + (int64_t)(u * kThreads + threadIdx.x) * 8));
-#pragma unroll
-      for (int u = 0; u < kGroups; ++u) {
-        const float4 f = widen4<DT>(make_uint2(g[u].x, g[u].y));
-        const float4 h = widen4<DT>(make_uint2(g[u].z, g[u].w));
-        acc += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
-        acc += h.x * h.x + h.y * h.y + h.z * h.z + h.w * h.w;
-      }
-    } else {
-      for (int u = 0; u < kGroups; ++u) {
-        const int64_t e0 = base + (int64_t)(u * kThreads + threadIdx.x) * 8;
-        for (int64_t e = e0; e < e0 + 8 && e < it.n; ++e) {
-          const float f = widen1<DT>(g16[e]);
-          acc += f * f;
-        }
-      }
-    }
-  }
-  const float s = block_sum(acc);
-  if (threadIdx.x == 0) partials[blockIdx.x] = b.accumulate ? partials[blockIdx.x] + s : s;
-}
-
-__global__ void __launch_bounds__(kThreads)
-sumsq_finalize_kernel(const float* __restrict__ partials, int n, CsStepState* st,
-                      int accumulate) {
-  __shared__ double red[kThreads];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < n; i += kThreads) acc += (double)partials[i];
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int w = kThreads / 2; w > 0; w >>= 1) {  // fixed-order tree: deterministic
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const float total = (float)red[0];
-    st->sumsq = accumulate ? st->sumsq + total : total;
-  }
-}
-
 __global__ void step_state_init_kernel(CsStepState* st, float loss_scale) {
   st->beta1_pow = 1.0;
   st->beta2_pow = 1.0;
@@ -389,10 +306,6 @@ extern "C" int cs_adam_variant(int v) {
   return adam_variant();
 }
 
-extern "C" int cs_sumsq_partials(void) {
-  const int sms = num_sms();
-  return sms > 0 ? sms * 4 : -1;
-}
 
 extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
                               const CsAdamHyper* hyper, const CsStepState* d_state,
@@ -476,73 +389,6 @@ extern "C" int cs_adam_chunks(const CsAdamItem* items, int n_items, int dtype,
     if (int e = launch_error("cs_adam_chunks")) return e;
   }
   return 0;
-}
-
-extern "C" int cs_grad_sumsq(const CsGradItem* items, int n_items, int dtype,
-                             float* d_partials, void* stream) {
-  if (n_items < 0 || (n_items > 0 && !items) || !d_partials ||
-      (dtype != CS_FP16 && dtype != CS_BF16)) {
-    cs::set_error("cs_grad_sumsq: invalid argument");
-    return CS_EINVAL;
-  }
-  if (n_items > CS_MAX_ITEMS) {
-    cs::set_error("cs_grad_sumsq: %d items > CS_MAX_ITEMS", n_items);
-    return CS_ETOOMANY;
-  }
-  const int grid = cs_sumsq_partials();
-  if (grid <= 0) {
-    cs::set_error("cs_grad_sumsq: no CUDA device");
-    return CS_EINVAL;
-  }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int first = 0;
-  bool wrote = false;
-  do {
-    GradBatch b;
-    b.n = 0;
-    b.accumulate = wrote ? 1 : 0;
-    int64_t tiles = 0;
-    int i = first;
-    for (; i < n_items && b.n < cs::kMaxBatch; ++i) {
-      const CsGradItem& it = items[i];
-      if (it.n < 0 || (it.n > 0 && !it.g16)) {
-        cs::set_error("cs_grad_sumsq: item %d invalid", i);
-        return CS_EINVAL;
-      }
-      if (!aligned(it.g16, 8)) {
-        cs::set_error("cs_grad_sumsq: item %d misaligned", i);
-        return CS_EALIGN;
-      }
-      if (it.n == 0) continue;  // takes no batch slot
-      b.item[b.n] = it;
-      b.tile_start[b.n] = tiles;
-      tiles += (it.n + kSumsqTile - 1) / kSumsqTile;
-      ++b.n;
-    }
-    first = i;  // resume where this batch stopped
-    b.tile_start[b.n] = tiles;
-    // launched even when empty so the partials are (re)initialised
-    if (dtype == CS_FP16)
-      grad_sumsq_kernel<CS_FP16><<<grid, kThreads, 0, s>>>(b, d_partials);
-    else
-      grad_sumsq_kernel<CS_BF16><<<grid, kThreads, 0, s>>>(b, d_partials);
-    cs::note_launches(1);
-    if (int e = launch_error("cs_grad_sumsq")) return e;
-    wrote = true;
-  } while (first < n_items);
-  return 0;
-}
-
-extern "C" int cs_sumsq_finalize(const float* d_partials, int n_partials,
-                                 CsStepState* d_state, int accumulate, void* stream) {
-  if (!d_partials || n_partials <= 0 || !d_state) {
-    cs::set_error("cs_sumsq_finalize: invalid argument");
-    return CS_EINVAL;
-  }
-  sumsq_finalize_kernel<<<1, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      d_partials, n_partials, d_state, accumulate);
-  cs::note_launches(1);
-  return launch_error("cs_sumsq_finalize");
 }
 
 extern "C" int cs_step_state_init(CsStepState* d_state, float init_loss_scale, void* stream) {

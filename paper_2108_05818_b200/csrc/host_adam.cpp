@@ -291,28 +291,80 @@ extern "C" int cs_adam_chunks_host_oop(const CsAdamItem* in, const CsAdamItem* o
 }
 
 namespace {
+// Host twin of K2 (sumsq.cu): the canonical per-item order, fp32 adds and
+// multiplies as separate rounded operations (no FMA; -ffp-contract=off).
+constexpr int64_t kSqTile = 8192;
+
 template <int DT>
-__attribute__((target("avx2,f16c"))) double sumsq_range(const uint16_t* g, int64_t n,
-                                                        int threads) {
-  double acc = 0.0;
-#pragma omp parallel for num_threads(threads) reduction(+ : acc) schedule(static)
-  for (int64_t e = 0; e < n; ++e) {
-    float f;
-    if (DT == CS_FP16) {
-      f = _cvtsh_ss(g[e]);
-    } else {
-      const uint32_t u = (uint32_t)g[e] << 16;
-      std::memcpy(&f, &u, 4);
+__attribute__((target("avx2,f16c"))) inline __m256 widen8(const uint16_t* p) {
+  const __m128i h = _mm_loadu_si128(reinterpret_cast<const __m128i*>(p));
+  if (DT == CS_FP16) return _mm256_cvtph_ps(h);
+  return _mm256_castsi256_ps(_mm256_slli_epi32(_mm256_cvtepu16_epi32(h), 16));
+}
+
+// the 8 warp partials of one zero-padded tile
+template <int DT>
+__attribute__((target("avx2,f16c"))) void tile_partials(const uint16_t* tile, float* out8) {
+  float lane[256];
+  for (int tau = 0; tau < 256; ++tau) {
+    __m256 a = _mm256_setzero_ps();
+    for (int u = 0; u < 4; ++u) {
+      const __m256 x = widen8<DT>(tile + (256 * u + tau) * 8);
+      a = _mm256_add_ps(a, _mm256_mul_ps(x, x));
     }
-    acc += (double)f * (double)f;
+    alignas(32) float aj[8];
+    _mm256_store_ps(aj, a);
+    lane[tau] = ((aj[0] + aj[1]) + (aj[2] + aj[3])) + ((aj[4] + aj[5]) + (aj[6] + aj[7]));
   }
-  return acc;
+  for (int w = 0; w < 8; ++w) {
+    float v[32];
+    std::memcpy(v, lane + 32 * w, sizeof(v));
+    for (int o = 16; o > 0; o >>= 1) {
+      float nv[32];
+      for (int l = 0; l < 32; ++l) nv[l] = v[l] + v[l ^ o];
+      std::memcpy(v, nv, sizeof(v));
+    }
+    out8[w] = v[0];
+  }
+}
+
+template <int DT>
+double item_sumsq(const uint16_t* g, int64_t n, int threads) {
+  const int64_t tiles = (n + kSqTile - 1) / kSqTile;
+  std::vector<float> part((size_t)tiles * 8);
+#pragma omp parallel for num_threads(threads) schedule(static)
+  for (int64_t t = 0; t < tiles; ++t) {
+    const int64_t base = t * kSqTile;
+    if (base + kSqTile <= n) {
+      tile_partials<DT>(g + base, part.data() + t * 8);
+    } else {
+      std::vector<uint16_t> pad(kSqTile, 0);
+      std::memcpy(pad.data(), g + base, (size_t)(n - base) * 2);
+      tile_partials<DT>(pad.data(), part.data() + t * 8);
+    }
+  }
+  // 32 groups of 256 strands (strand s folds q = s, s + 8192, ...), each
+  // group a fixed tree, the group values folded in order
+  const int64_t q_n = tiles * 8;
+  double total = 0.0;
+  for (int c = 0; c < 32; ++c) {
+    double d[256];
+    for (int r = 0; r < 256; ++r) {
+      double acc = 0.0;
+      for (int64_t q = 256 * c + r; q < q_n; q += 8192) acc += (double)part[q];
+      d[r] = acc;
+    }
+    for (int w = 128; w > 0; w >>= 1)
+      for (int r = 0; r < w; ++r) d[r] += d[r + w];
+    total += d[0];
+  }
+  return total;
 }
 }  // namespace
 
 extern "C" int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtype, double* out,
                                   int n_threads) {
-  if (n_items < 0 || (n_items > 0 && !items) || !out || (dtype != CS_FP16 && dtype != CS_BF16)) {
+  if (n_items < 0 || (n_items > 0 && (!items || !out)) || (dtype != CS_FP16 && dtype != CS_BF16)) {
     cs::set_error("cs_grad_sumsq_host: invalid argument");
     return CS_EINVAL;
   }
@@ -321,16 +373,14 @@ extern "C" int cs_grad_sumsq_host(const CsGradItem* items, int n_items, int dtyp
     return CS_EINVAL;
   }
   const int threads = cs::host_threads(n_threads);
-  double total = 0.0;
   for (int i = 0; i < n_items; ++i) {
     const uint16_t* g = static_cast<const uint16_t*>(items[i].g16);
-    if (items[i].n > 0 && !g) {
+    if (items[i].n < 0 || (items[i].n > 0 && !g)) {
       cs::set_error("cs_grad_sumsq_host: item %d invalid", i);
       return CS_EINVAL;
     }
-    total += dtype == CS_FP16 ? sumsq_range<CS_FP16>(g, items[i].n, threads)
-                              : sumsq_range<CS_BF16>(g, items[i].n, threads);
+    out[i] = dtype == CS_FP16 ? item_sumsq<CS_FP16>(g, items[i].n, threads)
+                              : item_sumsq<CS_BF16>(g, items[i].n, threads);
   }
-  *out = total;
   return 0;
 }

@@ -8,7 +8,7 @@ no CPU path for GPU-resident work.
 """
 
 import ctypes
-from typing import Optional, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 import torch
 
@@ -191,19 +191,21 @@ def adam_chunks_host_oop(items_in, items_out, hyper: AdamHyper, state: N.CsStepS
             "cs_adam_chunks_host_oop")
 
 
-def grad_sumsq_host(grads: Sequence[Tuple[torch.Tensor, int]], n_threads: int = 0) -> float:
-    """Sum of squares of host-resident fp16/bf16 gradients (double)."""
+def grad_sumsq_host(grads: Sequence[Tuple[torch.Tensor, int]], n_threads: int = 0) -> List[float]:
+    """K2's host twin: the canonical sum of squares S_i (double) of each
+    host-resident fp16/bf16 gradient prefix -- the same bits K2 writes for
+    the same bytes in HBM."""
     if not grads:
-        return 0.0
+        return []
     arr = (N.CsGradItem * len(grads))()
     for i, (g, n) in enumerate(grads):
         if g.is_cuda:
             raise ValueError("grad_sumsq_host needs host tensors")
         arr[i] = N.CsGradItem(g.data_ptr(), n)
-    out = ctypes.c_double(0.0)
-    N.check(N.load().cs_grad_sumsq_host(arr, len(grads), _code(grads[0][0].dtype),
-                                        ctypes.byref(out), int(n_threads)), "cs_grad_sumsq_host")
-    return out.value
+    out = (ctypes.c_double * len(grads))()
+    N.check(N.load().cs_grad_sumsq_host(arr, len(grads), _code(grads[0][0].dtype), out,
+                                        int(n_threads)), "cs_grad_sumsq_host")
+    return list(out)
 
 
 def _host_contig(*ts: torch.Tensor) -> None:
@@ -294,31 +296,46 @@ def embed_bwd_into(tokens: torch.Tensor, dout: torch.Tensor, gwte: torch.Tensor,
                                   _code(dout.dtype), _stream(stream)), "cs_embed_bwd")
 
 
-def sumsq_partials() -> int:
-    n = N.load().cs_sumsq_partials()
-    if n <= 0:
-        raise N.NativeError("cs_sumsq_partials: no device")
-    return n
-
-
-def grad_sumsq(grads: Sequence[Tuple[torch.Tensor, int]], partials: torch.Tensor,
-               stream: Optional[torch.cuda.Stream] = None,
-               dtype: Optional[torch.dtype] = None) -> None:
-    """K2: per-block partial sums of squares of the given gradient prefixes."""
+def _grad_items(grads):
     arr = (N.CsGradItem * max(len(grads), 1))()
     for i, (g, n) in enumerate(grads):
-        _need_cuda(g)
         arr[i] = N.CsGradItem(g.data_ptr(), n)
-    dt = _code(dtype if dtype is not None else grads[0][0].dtype)
-    N.check(N.load().cs_grad_sumsq(arr, len(grads), dt, ctypes.c_void_p(partials.data_ptr()),
+    return arr
+
+
+def sumsq_scratch(grads: Sequence[Tuple[torch.Tensor, int]]) -> int:
+    """Floats of K2 scratch the given gradient prefixes need."""
+    n = N.load().cs_sumsq_scratch(_grad_items(grads), len(grads))
+    if n < 0:
+        raise N.NativeError("cs_sumsq_scratch: invalid items")
+    return int(n)
+
+
+def grad_sumsq(grads: Sequence[Tuple[torch.Tensor, int]], scratch: torch.Tensor,
+               item_sums: torch.Tensor, slots: Optional[Sequence[int]] = None,
+               stream: Optional[torch.cuda.Stream] = None,
+               dtype: Optional[torch.dtype] = None) -> None:
+    """K2: the canonical sum of squares S_i of each gradient prefix, written
+    into ``item_sums[slots[i]]`` (float64, on the device)."""
+    for g, _ in grads:
+        _need_cuda(g)
+    if item_sums.dtype != torch.float64 or not item_sums.is_cuda:
+        raise ValueError("item_sums must be a float64 CUDA tensor")
+    arr = _grad_items(grads)
+    sl = None
+    if slots is not None:
+        sl = (ctypes.c_int * max(len(slots), 1))(*slots)
+    dt = _code(dtype if dtype is not None else (grads[0][0].dtype if grads else torch.float16))
+    N.check(N.load().cs_grad_sumsq(arr, len(grads), dt, sl, ctypes.c_void_p(scratch.data_ptr()),
+                                   scratch.numel(), ctypes.c_void_p(item_sums.data_ptr()),
                                    _stream(stream)), "cs_grad_sumsq")
 
 
-def sumsq_finalize(partials: torch.Tensor, state: StepState, accumulate: bool = False,
+def sumsq_finalize(item_sums: torch.Tensor, state: StepState,
                    stream: Optional[torch.cuda.Stream] = None) -> None:
-    N.check(N.load().cs_sumsq_finalize(ctypes.c_void_p(partials.data_ptr()), partials.numel(),
-                                       state.ptr, int(accumulate), _stream(stream)),
-            "cs_sumsq_finalize")
+    """state.sumsq = (float) of the slots of ``item_sums`` folded in order (double)."""
+    N.check(N.load().cs_sumsq_finalize(ctypes.c_void_p(item_sums.data_ptr()), item_sums.numel(),
+                                       state.ptr, _stream(stream)), "cs_sumsq_finalize")
 
 
 def adam_prepare(state: StepState, hyper: AdamHyper, max_grad_norm: float = 0.0,

@@ -100,9 +100,10 @@ def bench_size(n: int, iters: int, dtype=torch.float16, flush: Optional[L2Flush]
     state = K.StepState(dev)
     state.sumsq().fill_(1.0)
     K.adam_prepare(state, hyper)
-    partials = torch.empty(K.sumsq_partials(), device=dev)
+    scratch = torch.empty(K.sumsq_scratch([(p16, n)]), device=dev)
+    item_sums = torch.empty(1, dtype=torch.float64, device=dev)
     fns = {"adam": lambda: K.adam_chunks([(p16, p32, m, v, n)], hyper, state),
-           "sumsq": lambda: K.grad_sumsq([(p16, n)], partials)}
+           "sumsq": lambda: K.grad_sumsq([(p16, n)], scratch, item_sums)}
     if any(k in kernels for k in ("pack", "accumulate", "cast_pack", "master_init")):
         src16 = (torch.randn(n, device=dev, generator=g)).to(dtype)
         src32 = torch.randn(n, device=dev, generator=g)

@@ -413,21 +413,31 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             streams.append(self.d2h_stream)
         self.slabs = SlabPool(self.device, streams)
         self.state = K.StepState(self.device, init_loss_scale)
-        self.partials = torch.zeros(K.sumsq_partials() + 1, device=self.device)
+        # K2 (canonical per-item sums of squares): scratch partials, one
+        # double per item slot on the device, and the host slots' values
+        self._sq_scratch = torch.empty(0, device=self.device)
+        self._sq_items = torch.empty(0, dtype=torch.float64, device=self.device)
+        self._sq_host: Optional[torch.Tensor] = None
+        self._sq_host_ev: Optional[torch.cuda.Event] = None
 
     # -- wiring -------------------------------------------------------------------
 
     def attach(self, chunk_set: ChunkSet, partition: DpPartition, rank: int,
                params: Sequence[torch.nn.Parameter], shapes: Sequence[Tuple[int, ...]],
                embedding: Sequence[Tuple[torch.nn.Parameter, torch.Tensor, torch.Tensor,
-                                         torch.Tensor]] = ()) -> None:
+                                         torch.Tensor]] = (),
+               embedding_keys: Optional[Sequence[int]] = None) -> None:
         """Bind the layout, this rank's partition and the model's parameters
         (``params[tid]`` has shape ``shapes[tid]``); ``embedding`` lists the
-        non-chunked (param, master, m, v) quadruples updated in the same K1."""
+        non-chunked (param, master, m, v) quadruples updated in the same K1,
+        ``embedding_keys`` their place in K2's canonical order (wte 0, wpe 1,
+        untied head 2; default: list order)."""
         self.chunk_set, self.partition, self.rank = chunk_set, partition, rank
         self.params, self.shapes = list(params), list(shapes)
         self.offsets = chunk_set.element_offsets()
         self.embedding = list(embedding)
+        self.embedding_keys = (list(embedding_keys) if embedding_keys is not None
+                               else list(range(len(self.embedding))))
         self._bound: Dict[int, int] = {}  # tid -> chunk id its .data views
         self.init32: Dict[int, torch.Tensor] = {}
 
@@ -1126,8 +1136,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         self._gather_prefetched.clear()     # (their Works are still in _inflight)
         self.wait_collectives()             # reduce-scatters into local chunks landed
         self._host_state = None
-        emb_grads = []
-        for param, _, _, _ in self.embedding:
+        emb_grads = []  # (key, grad): the canonical slot order of non-chunked parameters
+        for (param, _, _, _), key in zip(self.embedding, self.embedding_keys):
             # the fused model writes the gradient over the weights (grad
             # overwrite); the plain model leaves it in .grad
             g = param.data if grad_in_data(param) else param.grad
@@ -1135,17 +1145,20 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 raise RuntimeError("non-chunked parameter has no gradient at ADAM")
             if self.comm is not None and self.comm.world > 1:
                 self.comm.all_reduce_avg(g)
-            emb_grads.append((g, g.numel()))
-        dev_items, host_items = [], []
-        for pos in self.partition.local_positions(self.rank):
+            emb_grads.append((key, g))
+        # K2 item slots: local positions ascending, then the non-chunked
+        # parameters by key (wte 0, wpe 1, untied head 2) wherever they live
+        dev_items, host_items = [], []  # (grad, n, slot)
+        local = self.partition.local_positions(self.rank)
+        for slot, pos in enumerate(local):
             chunk = cs.param_chunk(pos)
             n = chunk.used_elems
             if self.has(chunk, GPU):
                 self.wait_ready(chunk, GPU)
-                dev_items.append((self.tensor(chunk, GPU), n))
+                dev_items.append((self.tensor(chunk, GPU), n, slot))
             else:
                 self.wait_ready(chunk, CPU)
-                host_items.append((self.tensor(chunk, CPU), n))
+                host_items.append((self.tensor(chunk, CPU), n, slot))
         he = self.host_embedding
         dev_emb = he is not None and he.device_compute
         drained = []
@@ -1156,7 +1169,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     raise RuntimeError("embedding has no gradient at ADAM")
                 if self.comm is not None and self.comm.world > 1:
                     self.comm.all_reduce_avg(g)
-                emb_grads.append((g, g.numel()))
+                emb_grads.append((0, g))  # wte
                 drained.append(g)
         if he is not None and not dev_emb:
             if not he.grads_ready:
@@ -1166,19 +1179,13 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                     d = g16.to(self.device, non_blocking=True)
                     self.comm.all_reduce_avg(d)
                     g16.copy_(d)
-        host_extra = 0.0
-        if self.comm is None or self.comm.rank == 0:
-            dev_items += emb_grads  # replicated after the all-reduce: count once
+        if self.comm is None or self.comm.rank == 0:  # replicated: counted once
+            nc = [(key, g, True) for key, g in emb_grads]
             if he is not None and not dev_emb:
-                if self.comm is None or self.comm.world == 1:
-                    host_extra = he.grad_sumsq  # computed by the scatter, hit rows only
-                else:                           # averaged over ranks since: recount
-                    host_items += he.grad_items()
-        host = K.grad_sumsq_host(host_items, self.host_threads) if host_items else 0.0
-        host += host_extra
-        self.partials[-1:].fill_(host)
-        K.grad_sumsq(dev_items, self.partials[:-1], dtype=self.dtype)
-        K.sumsq_finalize(self.partials, self.state)
+                nc += [(key, g16, False) for key, (g16, _) in enumerate(he.grad_items())]
+            for k, (key, g, on_gpu) in enumerate(sorted(nc, key=lambda x: x[0])):
+                (dev_items if on_gpu else host_items).append((g, g.numel(), len(local) + k))
+        self._grad_sumsq(dev_items, host_items)
         if dev_emb:  # the weight gradients go up (`engine.py:214-219`, billed at BWD)
             he.drain_grads(drained, self.d2h_stream, self.compute)
             for param in he.device_params:
@@ -1216,6 +1223,35 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 K.pack([(flat, 0, param.grad.view(-1), flat.numel())])
                 param.grad = None
             self._pending.append((flat, master, m, v, flat.numel()))
+
+    def _grad_sumsq(self, dev_items, host_items) -> None:
+        """K2 over every local gradient in the canonical slot order: device
+        items on the GPU, host items by the host twin (same bits), folded in
+        slot order into the step state's sumsq -- the global norm does not
+        depend on where each gradient lives."""
+        n_slots = len(dev_items) + len(host_items)
+        if self._sq_items.numel() != n_slots:
+            self._sq_items = torch.zeros(n_slots, dtype=torch.float64, device=self.device)
+        if host_items:
+            sums = K.grad_sumsq_host([(g, n) for g, n, _ in host_items], self.host_threads)
+            if self._sq_host is None or self._sq_host.numel() < n_slots:
+                self._sq_host = torch.zeros(max(n_slots, 64), dtype=torch.float64,
+                                            pin_memory=True)
+            elif self._sq_host_ev is not None:
+                self._sq_host_ev.synchronize()  # the last upload has read the buffer
+            self._sq_host.zero_()
+            for (_, _, slot), v in zip(host_items, sums):
+                self._sq_host[slot] = v
+            self._sq_items.copy_(self._sq_host[:n_slots], non_blocking=True)
+            self._sq_host_ev = torch.cuda.Event()
+            self._sq_host_ev.record()
+        grads = [(g, n) for g, n, _ in dev_items]
+        need = K.sumsq_scratch(grads)
+        if self._sq_scratch.numel() < need:
+            self._sq_scratch = torch.empty(need, device=self.device)
+        K.grad_sumsq(grads, self._sq_scratch, self._sq_items,
+                     slots=[slot for _, _, slot in dev_items], dtype=self.dtype)
+        K.sumsq_finalize(self._sq_items, self.state)
 
     def init_optimizer_state(self, position: int, device: str) -> None:
         p32, m, v = (self.tensor(c, device) for c in self.chunk_set.os_triplet(position))

@@ -258,7 +258,8 @@ class ChunkTrainer:
             emb.append((p, master, torch.zeros_like(master), torch.zeros_like(master)))
         ex.attach(self.sim.chunk_set, self.sim.partition, rank,
                   self.model.chunk_parameters(), self.shapes,
-                  [(p, mst.view(-1), m.view(-1), v.view(-1)) for p, mst, m, v in emb])
+                  [(p, mst.view(-1), m.view(-1), v.view(-1)) for p, mst, m, v in emb],
+                  embedding_keys=self._emb_seed_offsets)
         ex.set_timeline(self.sim.timeline)
         self._init_weights(seed, emb)
         self.iteration = 0

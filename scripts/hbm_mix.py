@@ -44,14 +44,15 @@ def main():
     f32 = torch.empty(n, device=dev)
     m = torch.empty(n, device=dev)
     v = torch.empty(n, device=dev)
-    partials = torch.empty(K.sumsq_partials(), device=dev)
+    scratch = torch.empty(K.sumsq_scratch([(h, n)]), device=dev)
+    item_sums = torch.empty(1, dtype=torch.float64, device=dev)
     out = torch.empty((), device=dev, dtype=torch.float32)
     rows = [
         ("read_only torch.sum fp16", lambda: torch.sum(h, dim=0, dtype=torch.float32, out=out),
          2, 0),
         ("write_only fill_ fp32", lambda: f32.fill_(1.0), 0, 4),
         ("copy_ fp16 1:1", lambda: h2.copy_(h), 2, 2),
-        ("K2 grad_sumsq", lambda: K.grad_sumsq([(h, n)], partials), 2, 0),
+        ("K2 grad_sumsq", lambda: K.grad_sumsq([(h, n)], scratch, item_sums), 2, 0),
         ("K3 pack", lambda: K.pack([(h2, 0, h, n)]), 2, 2),
         ("K4 accumulate", lambda: K.pack([(h2, 0, h, n)], accumulate=True), 4, 2),
         ("K5 cast_pack", lambda: K.cast_pack([(h2, 0, f32, n)]), 4, 2),

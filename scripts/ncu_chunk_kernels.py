@@ -18,10 +18,11 @@ hyper = K.AdamHyper(lr=1e-4)
 state = K.StepState(dev)
 state.sumsq().fill_(1.0)
 K.adam_prepare(state, hyper)
-partials = torch.empty(K.sumsq_partials(), device=dev)
+scratch = torch.empty(K.sumsq_scratch([(p16, n)]), device=dev)
+item_sums = torch.empty(1, dtype=torch.float64, device=dev)
 torch.cuda.synchronize()
 K.adam_chunks([(p16, p32, m, v, n)], hyper, state)                  # K1
-K.grad_sumsq([(p16, n)], partials)                                   # K2
+K.grad_sumsq([(p16, n)], scratch, item_sums)                          # K2
 K.pack([(p16, 0, src16, n)])                                         # K3
 K.pack([(p16, 0, src16, n)], accumulate=True)                        # K4
 K.cast_pack([(p16, 0, src32, n)])                                    # K5

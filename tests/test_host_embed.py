@@ -46,8 +46,9 @@ def test_embed_fwd_bwd_bit_exact(native_lib, oracle_lib, dtype, B, S, V, H, rep)
     # the fused sum of squares = the squares of the written (rounded) gradients
     ref_sq = sum(float((t.double() ** 2).sum()) for t in (gwte, gwpe))
     assert sq == pytest.approx(ref_sq, rel=1e-12, abs=0.0)
-    assert sq == pytest.approx(K.grad_sumsq_host([(gwte.view(-1), V * H),
-                                                  (gwpe.view(-1), S * H)]), rel=1e-12)
+    # K2's host twin (fp32 lane sums in the canonical order) agrees to fp32 rounding
+    assert sq == pytest.approx(sum(K.grad_sumsq_host([(gwte.view(-1), V * H),
+                                                      (gwpe.view(-1), S * H)])), rel=1e-6)
     # deterministic for any thread count (row-order reduction)
     for threads in (1, 7):
         assert K.embed_bwd_host(tok, dout, gwte.clone(), gwpe.clone(), n_threads=threads) == sq

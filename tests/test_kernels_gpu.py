@@ -7,6 +7,8 @@ multi-item launches (> 256 items → several launches), unaligned slot
 offsets, fp16 and bf16, L2 and decoupled weight decay, and the skip path.
 """
 
+import random
+
 import numpy as np
 import pytest
 import torch
@@ -144,14 +146,57 @@ def test_adam_skip_restores_params_and_leaves_state(native_lib, oracle_lib, adam
         assert torch.equal(d16.cpu(), d32.cpu().to(dtype))  # the parameters are back
 
 
+def _sumsq(items, state, dtype=None, slots=None, n_slots=None):
+    scratch = torch.empty(max(K.sumsq_scratch(items), 1), device=DEV)
+    sums = torch.zeros(n_slots if n_slots is not None else len(items), dtype=torch.float64,
+                       device=DEV)
+    K.grad_sumsq(items, scratch, sums, slots=slots, dtype=dtype)
+    K.sumsq_finalize(sums, state)
+    return sums
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+def test_grad_sumsq_canonical_bit_exact(native_lib, oracle_lib, dtype):
+    """K2 = the C oracle's restatement of the canonical order, bit for bit,
+    per item (whole and ragged tiles, empty items, an item misaligned for
+    128-bit loads) and for the slot fold; = the host twin on the same bytes."""
+    O = oracle_lib
+    code = O.FP16 if dtype == torch.float16 else O.BF16
+    gen = torch.Generator().manual_seed(9)
+    base = (torch.randn(3 * 8192 + 9000, generator=gen) * 0.05).to(dtype)
+    host_items = [(base[:n], n) for n in (1, 8191, 8192, 8193, 3 * 8192 + 4100)]
+    host_items += [(base[:0], 0), (base[3:3 + 20000], 20000)]  # empty; 6-byte offset
+    dev = base.to(DEV)
+    items = [(dev[:n], n) for n in (1, 8191, 8192, 8193, 3 * 8192 + 4100)]
+    items += [(dev[:0], 0), (dev[3:3 + 20000], 20000)]
+    state = K.StepState(DEV)
+    sums = _sumsq(items, state, dtype=dtype).cpu().numpy()
+    want = [O.grad_sumsq_item(_bits16(t.contiguous()), code) if n else 0.0
+            for t, n in host_items]
+    assert sums.tobytes() == np.array(want, dtype=np.float64).tobytes()
+    assert K.grad_sumsq_host([(t.contiguous(), n) for t, n in host_items]) == list(sums)
+    assert np.float32(state.read().sumsq) == np.float32(O.sumsq_total(want))
+
+
+def test_grad_sumsq_slots_and_batches(native_lib, oracle_lib):
+    """Slot order is the fold order whatever the item order or the launch
+    batching (more items than one launch takes)."""
+    gen = torch.Generator().manual_seed(4)
+    grads = [(torch.randn(500 + 37 * i, generator=gen) * 0.1).half().to(DEV) for i in range(300)]
+    perm = list(range(300))
+    random.Random(1).shuffle(perm)
+    s1, s2 = K.StepState(DEV), K.StepState(DEV)
+    a = _sumsq([(g, g.numel()) for g in grads], s1)
+    b = _sumsq([(grads[i], grads[i].numel()) for i in perm], s2, slots=perm, n_slots=300)
+    assert torch.equal(a, b) and s1.read().sumsq == s2.read().sumsq
+
+
 def test_grad_sumsq_and_step_scalars_match_oracle(native_lib, oracle_lib):
     O = oracle_lib
     gen = torch.Generator().manual_seed(5)
     grads = [(torch.randn(n, generator=gen) * 3).half() for n in (1, 4097, 300000, 1 << 21)]
-    partials = torch.empty(K.sumsq_partials(), device=DEV)
     state = K.StepState(DEV, init_loss_scale=2.0)
-    K.grad_sumsq([(x.to(DEV), x.numel()) for x in grads], partials)
-    K.sumsq_finalize(partials, state)
+    _sumsq([(x.to(DEV), x.numel()) for x in grads], state)
     hyper = K.AdamHyper(lr=1e-3, betas=(0.9, 0.99))
     K.adam_prepare(state, hyper, max_grad_norm=1.0, dynamic_scale=True, growth_interval=1)
     st = state.read()
@@ -163,19 +208,16 @@ def test_grad_sumsq_and_step_scalars_match_oracle(native_lib, oracle_lib):
     for f in ("grad_scale", "step_size", "sqrt_bc2", "grad_norm", "loss_scale", "step", "skip",
               "beta1_pow", "beta2_pow"):
         assert getattr(st, f) == getattr(s, f), f
-    # determinism: same inputs, same partials, bit-identical sumsq
-    K.grad_sumsq([(x.to(DEV), x.numel()) for x in grads], partials)
-    K.sumsq_finalize(partials, state)
+    # determinism: same inputs, bit-identical sumsq
+    _sumsq([(x.to(DEV), x.numel()) for x in grads], state)
     assert state.read().sumsq == st.sumsq
 
 
 def test_grad_sumsq_detects_inf(native_lib):
     g = torch.randn(10000, device=DEV).half()
     g[1234] = float("inf")
-    partials = torch.empty(K.sumsq_partials(), device=DEV)
     state = K.StepState(DEV)
-    K.grad_sumsq([(g, g.numel())], partials)
-    K.sumsq_finalize(partials, state)
+    _sumsq([(g, g.numel())], state)
     assert not np.isfinite(state.read().sumsq)
 
 
@@ -387,11 +429,8 @@ def test_chunk_kernels_past_2pow31_elements(native_lib, oracle_lib):
     assert torch.equal(big[off + 3:off + 3 + 9001], src32.half())
     del big
     # K2 over all 2^31 + 13 elements vs a float64 torch reduction
-    partials = torch.empty(K.sumsq_partials() + 1, device=DEV)
-    partials[-1:].zero_()
-    K.grad_sumsq([(p16, n)], partials[:-1])
     st = K.StepState(DEV)
-    K.sumsq_finalize(partials, st)
+    _sumsq([(p16, n)], st)
     ref = float((p16.double() ** 2).sum())
     assert abs(float(st.sumsq().item()) - ref) <= 1e-5 * ref
 
@@ -501,10 +540,11 @@ def test_sumsq_and_pack_with_zero_length_items_across_batches(native_lib):
         if i % 5 == 0:
             items.append((g, 0))
     assert len(items) > 256 + 30
-    partials = torch.zeros(K.sumsq_partials() + 1, device=DEV)
-    K.grad_sumsq(items, partials[:-1], dtype=torch.float16)
+    st = K.StepState(DEV)
+    sums = _sumsq(items, st, dtype=torch.float16)
     want = sum(float((g.double() ** 2).sum()) for g in grads)
-    assert abs(float(partials[:-1].double().sum()) - want) <= 1e-4 * want  # fp32 partials
+    assert abs(float(sums.sum()) - want) <= 1e-6 * want
+    assert all(float(s) == 0.0 for (g, n), s in zip(items, sums.cpu()) if n == 0)
     for acc in (0, 1):
         dst = torch.zeros(sum(g.numel() for g in grads), dtype=torch.float16, device=DEV)
         pk, off = [], 0

@@ -573,3 +573,39 @@ def test_tied_model_under_a_cpu_embedding_plan_computes_it_on_the_gpu():
         c = CASES[case]
         ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
                      embedding_placement="cpu")
+
+
+@pytest.mark.parametrize("emb", ["gpu", "cpu"])
+def test_clipped_training_is_placement_invariant(emb):
+    """With max_grad_norm > 0 the clip coefficient comes from the global sum
+    of squares, which K2 and its host twin evaluate in one canonical order
+    whatever lives where: a tight-budget run (chunks evicted, optimizer state
+    and gradients of some positions in host DRAM) and an all-resident run --
+    and a CPU-placed embedding (host gradients) -- give bit-identical losses,
+    norms and parameters."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_tight"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 5)
+    out = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for name, hw in (("tight", HardwareSpec(**c["hardware"])),
+                         ("resident", HardwareSpec(gpu_count=1, gpu_bytes=180 * 10 ** 9))):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), hw, dtype=torch.float16,
+                              seed=0, max_grad_norm=1e-3, embedding_placement=emb,
+                              untied_head=True)
+            losses, norms = [], []
+            for t in toks:
+                losses.append(tr.step_host(t))
+                tr.finish_host_work()
+                norms.append(tr.step_state().grad_norm)
+            params = [tr.local_chunk_payload(p).cpu().clone()
+                      for p in range(tr.sim.chunk_set.positions)]
+            out[name] = (losses, norms, params, tr)
+    (l0, n0, p0, tight), (l1, n1, p1, _) = out["tight"], out["resident"]
+    assert tight.executor.stats.copies > 0 and tight.executor.stats.host_adam_items > 0
+    assert n0 == n1 and all(n > 1e-3 for n in n0)   # clipping engaged at every step
+    assert l0 == l1
+    for a, b in zip(p0, p1):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
