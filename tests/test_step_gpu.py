@@ -609,3 +609,31 @@ def test_clipped_training_is_placement_invariant(emb):
     assert l0 == l1
     for a, b in zip(p0, p1):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+def test_clipped_training_cpu_and_gpu_embedding_agree():
+    """Clipped training with the embedding on the CPU (host operator, host
+    gradients summed by K2's host twin) and on the GPU (device operator,
+    gradients summed by K2): bit-identical losses, norms and parameters."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
+    from paper_2108_05818_b200.trainer import ChunkTrainer
+    c = CASES["tiny_tight"]
+    schema = build_gpt_schema(**c["schema"])
+    toks = _tokens(schema, 4)
+    out = {}
+    with sdpa_kernel(SDPBackend.MATH):
+        for place in ("cpu", "gpu"):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0, max_grad_norm=1e-3,
+                              embedding_placement=place, untied_head=True)
+            losses, norms = [], []
+            for t in toks:
+                losses.append(tr.step_host(t))
+                tr.finish_host_work()
+                norms.append(tr.step_state().grad_norm)
+            params = [tr.local_chunk_payload(p).cpu().clone()
+                      for p in range(tr.sim.chunk_set.positions)]
+            out[place] = (losses, norms, params)
+    assert out["cpu"][0] == out["gpu"][0] and out["cpu"][1] == out["gpu"][1]
+    for a, b in zip(out["cpu"][2], out["gpu"][2]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
