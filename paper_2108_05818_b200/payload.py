@@ -390,6 +390,7 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         #: HBM slab (data_ptr) -> {side stream: completion event of its last copy there}
         self._side_use: Dict[int, Dict[int, "torch.cuda.Event"]] = {}
         self._host_read_events = os.environ.get("CS_HOST_READ_EVENTS", "1") != "0"
+        self.nvtx = False  # NVTX ranges around chunk moves and collectives
         self._stats_lock = threading.Lock()
         #: CPU-placed embedding operator (embedding.HostEmbedding) or None
         self.host_embedding = None
@@ -660,6 +661,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             cs.wait_stream(self.compute)
         if prior is not None:
             cs.wait_event(prior)
+        if self.nvtx:
+            torch.cuda.nvtx.range_push("%s>%s %d B" % (src, dst, d.numel() * d.element_size()))
         with torch.cuda.stream(cs):
             if after is not None:
                 after.wait()
@@ -673,6 +676,8 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
             d.copy_(s, non_blocking=True)
             done = torch.cuda.Event(enable_timing=self.time_copies)
             done.record(cs)
+        if self.nvtx:
+            torch.cuda.nvtx.range_pop()
         if src == CPU:
             self._host_reads[s.data_ptr()] = done
         for t in ((s,) if src == GPU else ()) + ((d,) if dst == GPU else ()):
@@ -984,7 +989,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
                 self.wait_ready(local, CPU)
                 mine.copy_(self.tensor(local, CPU), non_blocking=True)
         t0 = self._coll_start()
+        if self.nvtx:
+            torch.cuda.nvtx.range_push("all_gather group %d" % group.group_id)
         work = self.comm.all_gather_slab(slab, async_op=self.overlap_collectives, src=src)
+        if self.nvtx:
+            torch.cuda.nvtx.range_pop()
         if work is not None:
             self._inflight.append((work, (slab,)))
             if src is not None:
@@ -1083,7 +1092,11 @@ class ChunkPayloadExecutor(PayloadBackend, CollectiveBackend, StepExecutor):
         if out is None:
             out = torch.empty(cap, dtype=self.dtype, device=self.device)  # phantom owner
         t0 = self._coll_start()
+        if self.nvtx:
+            torch.cuda.nvtx.range_push("reduce_scatter_avg group %d" % group.group_id)
         work = self.comm.reduce_scatter_avg(out, slab, async_op=self.overlap_collectives)
+        if self.nvtx:
+            torch.cuda.nvtx.range_pop()
         self._coll_end("reduce_scatter_avg", slab, work, t0)
         if work is not None:  # overlaps the next groups' backward; waited at first use
             self._inflight.append((work, (slab, out)))

@@ -280,6 +280,9 @@ class ChunkTrainer:
         self._side = None
         self.graph_kernels_per_step = 0
         self.phase_seconds = {"fwd": 0.0, "bwd": 0.0, "adam": 0.0}
+        #: NVTX ranges per timeline event, chunk move and collective (CS_NVTX=1)
+        self.nvtx = os.environ.get("CS_NVTX", "0") == "1"
+        self.executor.nvtx = self.nvtx
 
     # -- initialisation ---------------------------------------------------------------
 
@@ -352,12 +355,16 @@ class ChunkTrainer:
         return report
 
     def _on_start(self, idx: int) -> None:
+        if self.nvtx:  # one NVTX range per timeline event (SURVEY §5 tracing)
+            torch.cuda.nvtx.range_push(self._events[idx].name)
         self.sim.engine.start_event(self._events[idx])
         self._check()
 
     def _on_finish(self, idx: int) -> None:
         self.sim.engine.finish_event(self._events[idx])
         self._check()
+        if self.nvtx:
+            torch.cuda.nvtx.range_pop()
 
     # -- the step -----------------------------------------------------------------------------
 
@@ -400,10 +407,14 @@ class ChunkTrainer:
             (loss * self.executor.state.loss_scale()).backward()
             t2 = time.perf_counter()
             adam = self._events[-1]
+            if self.nvtx:
+                torch.cuda.nvtx.range_push(adam.name)
             eng.start_event(adam)
             self._check()
             eng.finish_event(adam)
             self._check()
+            if self.nvtx:
+                torch.cuda.nvtx.range_pop()
         except torch.OutOfMemoryError as e:
             # a physical allocation failed outside the engine's hooks (the
             # model's activations): the same verdict at the current moment
