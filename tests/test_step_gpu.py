@@ -643,15 +643,17 @@ def test_nvtx_ranges_do_not_change_the_step():
     """CS_NVTX=1 brackets every timeline event, chunk move and collective in
     an NVTX range (host-side markers): an evicting run with them gives the
     same losses and ledgers."""
+    from torch.nn.attention import SDPBackend, sdpa_kernel
     from paper_2108_05818_b200.trainer import ChunkTrainer
     c = CASES["tiny_tight"]
     schema = build_gpt_schema(**c["schema"])
     toks = _tokens(schema, 3)
     out = []
-    for nvtx in (False, True):
-        tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
-                          dtype=torch.float16, seed=0, untied_head=True)
-        tr.nvtx = tr.executor.nvtx = nvtx
-        losses = [tr.step_host(t) for t in toks]
-        out.append((losses, [_ledger(r)["transfers"] for r in tr.reports]))
+    with sdpa_kernel(SDPBackend.MATH):
+        for nvtx in (False, True):
+            tr = ChunkTrainer(schema, PolicySpec(**c["policy"]), HardwareSpec(**c["hardware"]),
+                              dtype=torch.float16, seed=0, untied_head=True)
+            tr.nvtx = tr.executor.nvtx = nvtx
+            losses = [tr.step_host(t) for t in toks]
+            out.append((losses, [_ledger(r)["transfers"] for r in tr.reports]))
     assert out[0] == out[1]
