@@ -525,6 +525,19 @@ def decision_engine_timing(args, iters=3):
     return out
 
 
+def workload_config(args, world):
+    """The workload both arms are measured on (the reference arm runs a
+    bounded sample of it, described in its ``cpu_baseline.sample``)."""
+    return {"workload": "GPT-2 1B chunk-managed training step (configs[1])",
+            "model": "GPT L%d H%d heads%d S%d V%d (reference-shaped, 8 chunked "
+                     "tensors/layer)" % (args.layers, args.hidden, args.heads, args.seq,
+                                         args.vocab),
+            "global_batch": world * args.batch, "per_gpu_batch": args.batch,
+            "seq_len": args.seq, "chunk_capacity_elems": args.cap,
+            "parallelism": "zero-chunk-dp%d" % world,
+            "l2": "inputs larger than L2 (16 GB of chunk state streamed per step)"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -544,14 +557,14 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / len(secs), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": "GPT 1B chunk-managed training step (reference CPU path, "
-                               "bounded sample)", "model": "GPT L%d H%d" % (args.layers,
-                                                                             args.hidden),
-                   "per_step_sample_tokens": runner.tokens_per_step},
+        "config": workload_config(args, int(os.environ.get("WORLD_SIZE", "1"))),
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": runner.threads,
                          "kind": "port", "host": host_info(),
-                         "sample": "%d x %d tokens per step on the full model"
-                                   % (args.cpu_sample_batch, args.seq)},
+                         "sample": "%d x %d tokens per step on the full model (fp32 "
+                                   "torch-CPU fwd/bwd + C-oracle chunk Adam over every "
+                                   "parameter + the decision engine): a bounded sample of "
+                                   "the workload's %d x %d tokens per GPU"
+                                   % (args.cpu_sample_batch, args.seq, args.batch, args.seq)},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -726,16 +739,9 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": "GPT-2 1B chunk-managed training step (configs[1])",
-                   "model": "GPT L%d H%d heads%d S%d V%d (reference-shaped, 8 chunked "
-                            "tensors/layer)" % (args.layers, args.hidden, args.heads, S,
-                                                args.vocab),
-                   "global_batch": world * B, "per_gpu_batch": B, "seq_len": S,
-                   "chunk_capacity_elems": args.cap,
-                   "positions": trainer.sim.chunk_set.positions,
-                   "parallelism": "zero-chunk-dp%d" % world,
-                   "os_on_gpu": len(trainer.sim.engine.plan.os_positions_on_gpu),
-                   "l2": "inputs larger than L2 (16 GB of chunk state streamed per step)"},
+        "config": workload_config(args, world),
+        "layout": {"positions": trainer.sim.chunk_set.positions,
+                   "os_on_gpu": len(trainer.sim.engine.plan.os_positions_on_gpu)},
         "tflops_per_gpu": round(flops / (ms * 1e-3) / 1e12, 2),
         "tflops_frac_of_sustained_bf16": round(flops / (ms * 1e-3) / 1e12 / bf16_peak, 4),
         "roofline": {"kernel": "cs_adam_chunks (K1 fused chunk Adam)", "bound": "hbm",

@@ -22,6 +22,15 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+    # the same workload config as our arm's line (the sample is in cpu_baseline)
+    sys.path.insert(0, ROOT)
+    import bench
+    argv, sys.argv = sys.argv, ["bench.py"] + cmd[2:]
+    try:
+        args = bench.parse()
+    finally:
+        sys.argv = argv
+    assert d["config"] == bench.workload_config(args, 1)
 
 
 def test_reference_arm_is_rank0_only():
