@@ -1,4 +1,4 @@
-import sys, torch, numpy as np
+import sys, torch
 sys.path.insert(0, '.')
 from torch.nn.attention import SDPBackend, sdpa_kernel
 from paper_2108_05818_b200 import kernels as K

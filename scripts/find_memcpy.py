@@ -1,5 +1,5 @@
 """Which Python lines issue the step's device-to-device memcpys?"""
-import os, sys, collections
+import sys
 sys.path.insert(0, '.')
 import torch
 from torch.profiler import ProfilerActivity, profile

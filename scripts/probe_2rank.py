@@ -1,4 +1,4 @@
-import os, sys, torch, torch.distributed as dist, torch.multiprocessing as mp
+import os, torch, torch.distributed as dist, torch.multiprocessing as mp
 def run(rank, ws, backend, port):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
