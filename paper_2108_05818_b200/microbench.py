@@ -41,7 +41,10 @@ from . import kernels as K
 BYTES_PER_ELEM = {"adam": 28, "sumsq": 2, "pack": 4, "accumulate": 6, "cast_pack": 6,
                   "master_init": 14}
 L2_BYTES = 126 << 20
-LATENCY_BOUND_BELOW = 1 << 24  # elements
+#: below this many algorithmic bytes per call, a fixed ~7-15 us of launch and
+#: event cost (one launch for K1/K3-K6, three for the canonical K2) is >= 5 %
+#: of the time at the HBM peak: such rows are reported as latency-bound
+LATENCY_BOUND_BELOW_BYTES = 256 << 20
 
 
 def measured_peak_gbs() -> float:
@@ -125,7 +128,8 @@ def run(sizes_log2: List[int], iters: int, kernels=tuple(BYTES_PER_ELEM)) -> Lis
             gbs = BYTES_PER_ELEM[name] * n / (ms * 1e-3) / 1e9
             rows.append({"arm": "gpu", "kernel": name, "n": n, "ms": round(ms, 5),
                          "gbs": round(gbs, 1), "frac_of_measured_peak": round(gbs / peak, 4),
-                         "regime": "latency-bound" if n < LATENCY_BOUND_BELOW else "hbm",
+                         "regime": ("latency-bound" if BYTES_PER_ELEM[name] * n < LATENCY_BOUND_BELOW_BYTES
+                                    else "hbm"),
                          "l2": "read-flushed before every launch (cold, clean)"})
         torch.cuda.empty_cache()
     return rows
